@@ -1,0 +1,126 @@
+"""ctypes binding of libhprlp_b200.so (include/hprlp_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or ``make``)
+and loaded from this package directory.  There is no fallback: if the
+shared object is missing or no CUDA device is present, ``lib()`` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libhprlp_b200.so"
+LIB_PATH = os.path.join(HERE, LIB_NAME)
+
+HPR_OPTIMAL, HPR_ITERATION_LIMIT, HPR_TIME_LIMIT, HPR_NUMERICAL_FAILURE = 0, 1, 2, 3
+HPR_FP64, HPR_FP32 = 0, 1
+HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
+
+EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
+           "hpr_destroy", "hpr_solve", "hpr_get_log", "hpr_matvec", "hpr_kkt_residual",
+           "hpr_power_method", "hpr_iterate")
+
+_p = C.c_void_p
+
+
+class Problem(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32), ("n_eq", C.c_int32), ("nnz", C.c_int64),
+                ("indptr", _p), ("indices", _p), ("data", _p),
+                ("t_indptr", _p), ("t_indices", _p), ("t_data", _p),
+                ("rhs", _p), ("cost", _p), ("lower", _p), ("upper", _p),
+                ("offset", C.c_double)]
+
+
+class Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stream", _p), ("workspace", _p),
+                ("workspace_bytes", C.c_size_t)]
+
+
+class Params(C.Structure):
+    _fields_ = [("tolerance", C.c_double), ("max_iterations", C.c_int64),
+                ("time_limit", C.c_double), ("time_elapsed", C.c_double),
+                ("precision", C.c_int32), ("has_sigma0", C.c_int32), ("sigma0", C.c_double),
+                ("restart_beta", C.c_double), ("restart_stall", C.c_int64),
+                ("sigma_damping", C.c_double), ("ruiz", C.c_int32), ("ruiz_iters", C.c_int32),
+                ("pock_chambolle", C.c_int32), ("normalize_rhs_objective", C.c_int32),
+                ("check_every", C.c_int32), ("power_tol", C.c_double),
+                ("power_inflation", C.c_double), ("power_max_iter", C.c_int32),
+                ("power_start", _p), ("power_start_count", C.c_int32),
+                ("log_residuals", C.c_int32), ("log_every_iteration", C.c_int32)]
+
+
+class Kkt(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("primal", "box", "dual", "rel_primal", "rel_box",
+                                          "rel_dual", "primal_objective", "dual_objective",
+                                          "gap", "rel_gap")]
+
+
+class Stats(C.Structure):
+    _fields_ = [("status", C.c_int32), ("precision_used", C.c_int32),
+                ("iterations", C.c_int64), ("restarts", C.c_int64),
+                ("sigma_final", C.c_double), ("lam", C.c_double), ("objective", C.c_double),
+                ("kkt", Kkt), ("n_log", C.c_int64), ("power_iterations", C.c_int32),
+                ("power_converged", C.c_int32), ("setup_seconds", C.c_double),
+                ("loop_seconds", C.c_double), ("gpu_launches", C.c_int64),
+                ("checks", C.c_int64)]
+
+
+class LogRecord(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("epoch", C.c_int64), ("k", C.c_int64)] + [
+        (k, C.c_double) for k in ("rel_primal", "rel_dual", "rel_box", "rel_gap", "sigma",
+                                  "primal", "box", "dual")]
+
+
+class HprError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libhprlp_b200 error {code}: {msg}")
+        self.code = code
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library and declare signatures (no device needed)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build() (or make) first")
+    lib = C.CDLL(path)
+    lib.hpr_abi_version.restype = C.c_int32
+    lib.hpr_last_error.restype = C.c_char_p
+    lib.hpr_workspace_bytes.argtypes = [C.POINTER(Problem), C.POINTER(C.c_size_t)]
+    lib.hpr_create.argtypes = [C.POINTER(Problem), C.POINTER(Options), C.POINTER(_p)]
+    lib.hpr_destroy.argtypes = [_p]
+    lib.hpr_destroy.restype = None
+    lib.hpr_solve.argtypes = [_p, C.POINTER(Params), _p, _p, _p, _p, _p, _p, C.POINTER(Stats)]
+    lib.hpr_get_log.argtypes = [_p, C.POINTER(LogRecord), C.c_int64, C.POINTER(C.c_int64)]
+    lib.hpr_matvec.argtypes = [_p, C.c_int32, _p, _p]
+    lib.hpr_kkt_residual.argtypes = [_p, _p, _p, _p, C.POINTER(Kkt)]
+    lib.hpr_power_method.argtypes = [_p, C.c_double, C.c_int32, C.c_double, _p, C.c_int32,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32)]
+    lib.hpr_iterate.argtypes = [_p, C.c_int32, C.c_double, C.c_double, C.c_int64] + [_p] * 12
+    _LIB = lib
+    return lib
+
+
+def check(code: int):
+    if code != 0:
+        msg = load().hpr_last_error().decode(errors="replace")
+        raise HprError(code, msg)
+
+
+def ptr(a) -> C.c_void_p | None:
+    """Address of a contiguous numpy array or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return C.c_void_p(a.ctypes.data)
+    return C.c_void_p(a.data_ptr())

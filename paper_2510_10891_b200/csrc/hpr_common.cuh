@@ -1,0 +1,88 @@
+// hpr_common.cuh — shared device types and numpy-faithful scalar helpers.
+//
+// The HPR engine reproduces the reference's numpy arithmetic operation by
+// operation (scuckit/hprlp.py:184-207 and :98-139), so the elementwise
+// helpers below follow numpy's semantics exactly: np.maximum/np.minimum
+// propagate NaN, Python-float scalars are cast to the work dtype before
+// use (NEP 50 weak scalars), and this file is compiled with -fmad=false so
+// no product is fused into a following add.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hpr {
+
+constexpr int TPB = 256;          // threads per CTA for every tiled kernel
+constexpr int TILE_NNZ = 2048;    // nonzeros staged per stream tile (16 KB FP64 products)
+constexpr int TILE_ROWS = 1024;   // rows per stream tile
+constexpr int ITEMS = TILE_NNZ / TPB;
+constexpr int CHUNK_NNZ = 4096;   // nonzeros per CTA on a long (split) row
+constexpr int MAX_B = 64;         // largest check_every the fused loop body supports
+
+// quantities accumulated by the two master-space check kernels
+constexpr int KR = 4;   // rows: primal^2, rhs.y, dy^2, nonfinite(bar_y)
+constexpr int KC = 7;   // cols: dual^2, box^2, cost.x, lo-terms, up-terms, dx^2, nonfinite(bar_x,bar_z)
+
+// np.maximum / np.minimum (NaN-propagating, first operand wins ties)
+template <typename T> __device__ __forceinline__ T np_max(T a, T b) { return (a >= b || a != a) ? a : b; }
+template <typename T> __device__ __forceinline__ T np_min(T a, T b) { return (a <= b || a != a) ? a : b; }
+template <typename T> __device__ __forceinline__ T np_clip(T x, T lo, T hi) { return np_min(np_max(x, lo), hi); }
+__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+__device__ __forceinline__ bool finite(float v) { return isfinite(v); }
+
+// streaming (evict-first) loads for the matrix stream; the gathered vectors
+// stay in L2 (126 MB) while A and A^T stream from HBM.
+template <typename T> __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+template <typename T> __device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }
+
+// Solver control block, resident in device memory for the whole solve.  The
+// iteration kernels read sigma/lam/k0 from it; the controller kernel owns it.
+struct Ctrl {
+    // HPR state scalars (HprState, hprlp.py:142-181)
+    double sigma, lam, norm_a;
+    long long k0;                 // in-epoch counter at the start of the current block
+    long long total;              // total iterations at the start of the current block
+    long long epoch, restarts, last_improvement;
+    double last_restart_res, epoch_min;
+    // KKT of the best and the latest check: primal, box, dual, rel_p, rel_b, rel_d, pobj, dobj, gap, rel_gap
+    double best[10];
+    double cur[10];
+    // configuration
+    double tol, beta, damping, denom, offset, b_scale, c_scale;
+    long long max_iter, stall, B;
+    unsigned long long deadline_ns;
+    int has_deadline;
+    int status;                   // -1 running, else HPR_* status
+    int flag_improved, flag_restart;
+    long long checks;
+    // logging
+    long long n_log, log_cap;
+    int log_on;
+    unsigned long long cond;      // cudaGraphConditionalHandle (0 when not in a graph)
+    // power method / setup scratch
+    double scratch[8];
+};
+
+struct LogRec {
+    long long iteration, epoch, k;
+    double rel_primal, rel_dual, rel_box, rel_gap, sigma;
+    double primal, box, dual;
+};
+
+// A CSR operand in device memory plus its tile schedule.
+template <typename T>
+struct Csr {
+    int rows, cols;
+    const int* indptr;
+    const int* indices;
+    const T* vals;
+    const int4* tiles;       // {r0, r1, lanes, -1} stream tile | {row, e0, e1, long_idx} chunk
+    int ntiles;
+    const int4* longs;       // {row, first_tile, nchunks, 0}
+    int nlong;
+    int* counters;           // per long row, zero between launches
+    double* tile_part;       // per tile partial sums of long-row chunks
+};
+
+}  // namespace hpr

@@ -1,0 +1,71 @@
+"""The vectorised SCUC LP builder reproduces the reference build_model."""
+
+import numpy as np
+import pytest
+
+from paper_2510_10891_b200 import scuc
+from tests.conftest import needs_reference
+
+
+def sizes(doc, n_mon):
+    G, B, T = len(doc["generators"]), len(doc["buses"]), doc["time_periods"]
+    H = sum(len(g["segments"]) for g in doc["generators"])
+    return dict(n=5 * G * T + T * H + B * T, n_eq=3 * G * T + T,
+                m=9 * G * T + T + T * H + 2 * n_mon)
+
+
+@pytest.mark.parametrize("args", [(6, 5, 8, 6, 0), (30, 12, 45, 8, 3), (60, 20, 90, 12, 7)])
+def test_size_formulas(args):
+    B, G, L, T, seed = args
+    doc = scuc.generate_instance(B, G, L, T, seed=seed)
+    mon = scuc.sample_monitored(doc, 10, seed)
+    lp = scuc.build_relaxation(doc, mon)
+    s = sizes(doc, len(set(mon)))
+    assert lp.shape == (s["m"], s["n"]) and lp.n_eq == s["n_eq"]
+    # flow row pairs are exact negatives (formulation.py:366-369)
+    csr = lp.csr()
+    lo = csr[lp.shape[0] - 2].toarray()
+    hi = csr[lp.shape[0] - 1].toarray()
+    assert np.array_equal(lo, -hi)
+
+
+def test_generator_is_deterministic():
+    a = scuc.generate_instance(30, 12, 45, 8, seed=3)
+    b = scuc.generate_instance(30, 12, 45, 8, seed=3)
+    assert a == b
+    la = scuc.build_relaxation(a, scuc.all_base_triples(a))
+    lb = scuc.build_relaxation(b, scuc.all_base_triples(b))
+    assert la.digest() == lb.digest()
+
+
+@needs_reference
+@pytest.mark.parametrize("args", [(6, 5, 8, 6, 0, -1), (30, 12, 45, 8, 3, -1),
+                                  (60, 20, 90, 12, 7, 40), (118, 54, 186, 24, 1, 300)])
+def test_csr_identical_to_reference_build_model(args):
+    from scuckit import build_model, parse_instance
+    B, G, L, T, seed, ntr = args
+    doc = scuc.generate_instance(B, G, L, T, seed=seed)
+    mon = scuc.all_base_triples(doc) if ntr < 0 else scuc.sample_monitored(doc, ntr, seed)
+    mine = scuc.build_relaxation(doc, mon)
+    ref = build_model(parse_instance(doc), monitored=mon)[0].relax()
+    c = ref.matrix.csr
+    assert c.shape == mine.shape and ref.n_eq == mine.n_eq
+    assert np.array_equal(c.indptr, mine.indptr) and np.array_equal(c.indices, mine.indices)
+    assert np.array_equal(c.data, mine.data)
+    for a, b in ((ref.rhs, mine.rhs), (ref.cost, mine.cost), (ref.lower, mine.lower),
+                 (ref.upper, mine.upper)):
+        assert np.array_equal(a, b)
+
+
+@needs_reference
+def test_direct_ptdf_rows_match_reference_tables():
+    from scuckit import compute_ptdf, parse_instance
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7, n_contingencies=3)
+    inst = scuc.Instance(doc)
+    ref = compute_ptdf(parse_instance(doc).network)
+    lines = [0, 5, 70, 89]
+    for key in ["base"] + [c["id"] for c in doc["contingencies"]]:
+        skip = None if key == "base" else inst.net.cont_line[key]
+        rows = scuc._ptdf_rows_direct(inst.B, inst.net.fb, inst.net.tb, inst.net.react,
+                                      inst.net.ref, lines, skip=skip)
+        np.testing.assert_allclose(rows, ref.table(key)[lines], rtol=0, atol=1e-12)

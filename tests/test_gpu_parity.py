@@ -1,0 +1,183 @@
+"""GPU parity: the sm_100a engine (through the C-ABI) against the golden
+reference vectors and the CPU oracle on identical inputs."""
+
+import numpy as np
+import pytest
+
+from oracle import hpr_oracle as O
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2510_10891_b200 import hprlp
+    return hprlp
+
+
+def _one_d():
+    return golden_io.FixtureLp(np.array([0, 1]), np.array([0]), np.array([1.0]), (1, 1), [1.0],
+                               [1.0], [0.0], [2.0], 0)
+
+
+def test_kat_iterate_and_kkt(H):
+    k = golden_io.kat()
+    lp = _one_d()
+    st = H.HprState.from_point([1.0], [1.0], [0.0], sigma=1.0, lam=1.0)
+    H.hpr_iterate(st, lp)
+    assert [st.x[0], st.y[0], st.z[0]] == k["fixed_point_after"]
+    r = H.kkt_residual(np.array([1.0]), np.array([1.0]), np.array([0.0]), lp)
+    assert [r.primal, r.box, r.dual] == [0.0, 0.0, 0.0]
+    st = H.HprState.from_point([0.0], [0.0], [0.0], sigma=1.0, lam=1.0)
+    H.hpr_iterate(st, lp)
+    assert [st.bar_x[0], st.bar_y[0], st.bar_z[0]] == k["from_zero_bar"]
+    assert [st.x[0], st.y[0], st.z[0]] == k["from_zero_next"]
+    assert H.kkt_residual(np.array([0.5]), np.array([0.0]), np.array([0.0]), lp).primal == 0.5
+
+
+def test_kat_power_and_solve(H):
+    import scipy.sparse as sp
+    from paper_2510_10891_b200.lp import SparseMatrix
+    k = golden_io.kat()
+    assert H.power_method(SparseMatrix(sp.eye(3))) == pytest.approx(k["power_identity"], rel=1e-15)
+    assert H.power_method(SparseMatrix(sp.diags([2.0, 1.0]))) == pytest.approx(
+        k["power_diag21"], rel=1e-12)
+    r = H.solve(_one_d(), H.SolverConfig(tolerance=1e-8))
+    g = k["one_d_solve"]
+    assert r.status.value == g["status"] and r.iterations == g["iterations"]
+    assert r.objective == pytest.approx(g["objective"], rel=1e-12)
+
+
+def test_matvec_matches_scipy(H):
+    from paper_2510_10891_b200 import scuc
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7)
+    lpa = scuc.build_relaxation(doc, scuc.sample_monitored(doc, 200, 7))
+    lp = lpa.to_lp()
+    eng = H.engine_for(lp)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(lpa.shape[1])
+    y = rng.standard_normal(lpa.shape[0])
+    csr = lpa.csr()
+    np.testing.assert_allclose(eng.matvec(x), csr @ x, rtol=1e-13, atol=1e-12)
+    np.testing.assert_allclose(eng.matvec(y, transpose=True), csr.T @ y, rtol=1e-13, atol=1e-12)
+    # <Ax, y> = <x, A^T y>
+    assert abs(eng.matvec(x) @ y - x @ eng.matvec(y, transpose=True)) <= 1e-11 * (
+        np.linalg.norm(x) * np.linalg.norm(y) * abs(csr).max())
+
+
+CFGS = {"fp64": dict(tolerance=1e-8), "fp32": dict(tolerance=1e-6, precision="fp32"),
+        "fp64_noruiz_log": dict(tolerance=1e-6, ruiz=False, log_residuals=True)}
+
+
+def _cfg(H, d):
+    d = dict(d)
+    if "precision" in d:
+        from paper_2510_10891_b200.lp import Precision
+        d["precision"] = Precision(d["precision"])
+    return H.SolverConfig(**d)
+
+
+@pytest.mark.parametrize("tag", list(CFGS))
+def test_random_lps_vs_reference(H, tag):
+    worst = 0.0
+    same_traj = 0
+    for lp, rec, res in golden_io.random_lps():
+        g = res[tag]
+        r = H.solve(lp, _cfg(H, CFGS[tag]))
+        assert r.status.value == g["status"]
+        tol = 1e-6 if tag != "fp32" else 1e-4
+        rel = abs(r.objective - g["objective"]) / max(1.0, abs(g["objective"]))
+        worst = max(worst, rel)
+        assert rel <= tol, (r.objective, g["objective"])
+        assert r.lam == pytest.approx(g["lam"], rel=1e-12 if tag != "fp32" else 1e-12)
+        same_traj += (r.iterations, r.restarts) == (g["iterations"], g["restarts"])
+        if tag == "fp64":
+            assert abs(r.objective - rec["highs_objective"]) <= 1e-6 * max(
+                1.0, abs(rec["highs_objective"]))
+    # FP64 trajectories are robust to summation order: nearly all identical
+    assert same_traj >= (22 if tag != "fp32" else 12), same_traj
+
+
+def test_scuc_small_trajectory(H):
+    lp, meta, res = golden_io.scuc_small()
+    g = res["fp64_1e4"]
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-4, ruiz=False, log_residuals=True))
+    assert r.status.value == g["status"]
+    assert r.lam == pytest.approx(g["lam"], rel=1e-12)
+    assert abs(r.objective - g["objective"]) <= 1e-6 * abs(g["objective"])
+    assert abs(r.iterations - g["iterations"]) <= 0.02 * g["iterations"]
+    mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"], e["rel_box"],
+                      e["rel_gap"], e["sigma"]] for e in r.residual_log])
+    k = min(len(mine), len(g["log"]), 200)
+    np.testing.assert_allclose(mine[:k], g["log"][:k], rtol=1e-6)
+
+
+def test_scuc_small_ruiz_window(H):
+    lp, meta, res = golden_io.scuc_small()
+    g = res["fp64_1e6_ruiz"]
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-6, ruiz=True, log_residuals=True,
+                                   max_iterations=20000))
+    assert r.status.value == g["status"] and r.iterations == 20000
+    assert r.lam == pytest.approx(g["lam"], rel=1e-12)
+    assert abs(r.objective - g["objective"]) <= 1e-6 * abs(g["objective"])
+    mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"], e["rel_box"],
+                      e["rel_gap"], e["sigma"]] for e in r.residual_log])
+    np.testing.assert_allclose(mine[:300], g["log"][:300], rtol=1e-6)
+
+
+def test_scuc_vs_oracle_on_box(H):
+    """Same seeded LP built on the box; GPU and oracle from the same inputs."""
+    from paper_2510_10891_b200 import scuc
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7)
+    lpa = scuc.build_relaxation(doc, scuc.sample_monitored(doc, 200, 7))
+    for prec, cfg in (("fp64", dict(tolerance=1e-4, ruiz=False, log_residuals=True)),
+                      ("fp64", dict(tolerance=1e-5, ruiz=True, log_residuals=True)),
+                      ("fp32", dict(tolerance=1e-4, ruiz=False, log_residuals=True))):
+        ref = O.solve(lpa, O.OracleConfig(precision=prec, **cfg))
+        r = H.solve(lpa.to_lp(), _cfg(H, dict(precision=prec, **cfg)))
+        assert r.status.value == ref.status
+        assert r.lam == pytest.approx(ref.lam, rel=1e-12)
+        tol = 1e-6 if prec == "fp64" else 1e-4
+        assert abs(r.objective - ref.objective) <= tol * abs(ref.objective)
+        if prec == "fp64":
+            assert abs(r.iterations - ref.iterations) <= max(32, 0.02 * ref.iterations)
+
+
+def test_warm_start_at_optimum_converges_immediately(H):
+    lp, rec, res = golden_io.random_lps()[3]
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-6))
+    r2 = H.solve(lp, H.SolverConfig(tolerance=1e-6), start=(r.x, r.y, r.z))
+    assert r2.iterations == 0 and r2.converged
+    o = O.solve(lp, O.OracleConfig(tolerance=1e-6), start=(r.x, r.y, r.z))
+    assert o.iterations == 0
+
+
+def test_limits_and_errors(H):
+    lp, rec, res = golden_io.random_lps()[1]
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-12, max_iterations=37))
+    assert r.status.value == "iteration-limit" and r.iterations == 37
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-14, max_iterations=10**7, time_limit=0.2))
+    assert r.status.value == "time-limit"
+    with pytest.raises(ValueError):
+        H.SolverConfig(tolerance=0.0)
+    z = golden_io.FixtureLp(np.array([0, 0]), np.array([], int), np.array([]), (1, 1), [1.0],
+                            [1.0], [0.0], [2.0], 0)
+    with pytest.raises(ValueError):
+        H.solve(z)
+
+
+def test_log_every_iteration_rate_log(H):
+    lp, rec, res = golden_io.random_lps()[2]
+    cfg = dict(tolerance=1e-6, log_every_iteration=True)
+    r = H.solve(lp, H.SolverConfig(**cfg))
+    o = O.solve(lp, O.OracleConfig(**cfg))
+    assert r.iterations == o.iterations
+    assert len(r.rate_log) == len(o.rate_log)
+    a = np.array(r.rate_log)
+    b = np.array(o.rate_log)
+    np.testing.assert_array_equal(a[:, :2], b[:, :2])
+    np.testing.assert_allclose(a[:, 2], b[:, 2], rtol=1e-8, atol=1e-14)
