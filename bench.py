@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""HPR-LP benchmark on the synthetic 13,659-bus SCUC LP relaxation.
+
+Workload (BASELINE.json configs[3], SURVEY.md §8(d) "C4"): 13,659 buses,
+4,092 units, 20,467 lines, 36 periods, 1,000 seeded base-case flow triples;
+the LP relaxation of the SCUC MILP (1.77M rows x 1.67M cols, ~44M nnz)
+built by paper_2510_10891_b200.scuc (random-init data, no datasets).
+
+A *step* is one HPR check block: 16 fused iterations + the master-space
+KKT check / restart controller (hprlp.py:393-446), device-resident.
+`value` = HPR iterations/s over K steps (CUDA events on the engine stream,
+max over ranks).  `e2e` = the same metric through the public API
+(hprlp.solve from host numpy arrays: upload, setup, solve to 1e-4, copy
+back).  The matrix stream (>1 GB per iteration) exceeds L2, so no flush is
+needed between steps.
+
+    python bench.py [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N     (independent replicas)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HPR iterations/s (time-to-1e-4 KKT in e2e) on 13659-bus SCUC LP"
+BLOCK = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--triples", type=int, default=None)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--e2e-max-iter", type=int, default=200_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel_key):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture summary (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(kernel_key)
+    except Exception:
+        return None
+
+
+def build_lp(args, device):
+    from paper_2510_10891_b200 import scuc
+    t = time.perf_counter()
+    doc, mon, lpa = scuc.build_config(args.config, n_triples=args.triples, device=device)
+    return lpa, time.perf_counter() - t
+
+
+def bytes_model(m, n, nnz, s):
+    """Algorithmic HBM bytes: per fused SpMV launch, per
+    iteration (core), per master check, and B_iter = core + check/16."""
+    k_dual = nnz * (s + 4) + 4 * (m + 1) + s * n + s * 4 * m          # A x~ gather + y,rhs,ya r/w
+    k_primal = nnz * (s + 4) + 4 * (n + 1) + s * m + s * 10 * n       # A^T y gather + 10 n vectors
+    core = 2 * nnz * (s + 4) + 4 * (m + n + 2) + s * (11 * n + 5 * m)
+    chk = 2 * nnz * 12 + 4 * (m + n + 2) + 8 * (8 * n + 4 * m) + 8 * (2 * n + m)
+    return {"k_dual": k_dual, "k_primal": k_primal, "core": core, "check": chk,
+            "iter": core + chk / BLOCK}
+
+
+def cpu_baseline_sample(lpa, lam, sigma, precision):
+    """The oracle (numpy/scipy restatement of the reference, single-threaded
+    SpMV) timed on one HPR block of the same LP: 16 iterations + 1 check,
+    after its own scaling (setup excluded; lambda/sigma from the GPU run)."""
+    from oracle import hpr_oracle as O
+    cfg = O.OracleConfig(tolerance=1e-4, ruiz=False, precision=precision)
+    p = O.Problem.from_lp(lpa)
+    sc = O.Scaling(p, cfg)
+    w = sc.work
+    dt = cfg.dtype
+    if dt == np.float32:
+        w = O.Problem(w.a.cast(np.float32), w.rhs.astype(dt), w.cost.astype(dt),
+                      w.lower.astype(dt), w.upper.astype(dt), w.n_eq)
+    m, n = p.a.shape
+    st = O.HprIterate(O.box(np.zeros(n), sc.work.lower, sc.work.upper), np.zeros(m), np.zeros(n),
+                      sigma, lam, dt)
+    t0 = time.perf_counter()
+    for _ in range(BLOCK):
+        st.step(w)
+    O.kkt(p, *sc.to_master(st.bx, st.by, st.bz))
+    el = time.perf_counter() - t0
+    return BLOCK / el, el
+
+
+def run_b200(args):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_10891_b200 import hprlp
+    from paper_2510_10891_b200.lp import Precision
+
+    lpa, t_build = build_lp(args, f"cuda:{local}")
+    m, n = lpa.shape
+    nnz = lpa.nnz
+    s = 8 if args.precision == "fp64" else 4
+    lp = lpa.to_lp()
+    eng = hprlp.Engine(lp, device=local)
+    cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(args.precision),
+                             max_iterations=max(1, args.warmup) * BLOCK)
+    x, y, z, st0, _ = eng.solve_raw(cfg)                  # setup + W warm-up blocks
+    # timed region: exactly K blocks of the device-resident loop
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        st = eng.resume(args.steps * BLOCK, tolerance=1e-300)
+        torch.cuda.synchronize()
+        k_dual = eng.bench_kernel(0, args.kernel_reps)
+        k_primal = eng.bench_kernel(1, args.kernel_reps)
+    if ws > 1:
+        torch.distributed.barrier()
+    t_loop = st.loop_seconds
+    its = int(st.iterations)
+    if ws > 1:
+        tt = torch.tensor([t_loop], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_loop = float(tt.item())
+    value = ws * its / t_loop
+
+    bm = bytes_model(m, n, nnz, s)
+    peak, peak_kind = measured_peak_hbm()
+    dom, dom_t, dom_b = (("k_dual", k_dual, bm["k_dual"]) if k_dual >= k_primal
+                         else ("k_primal", k_primal, bm["k_primal"]))
+    ach = dom_b / dom_t / 1e9
+    traffic = ncu_traffic(f"{dom}_{args.precision}")
+    it_gbs = bm["iter"] * its / t_loop / 1e9
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_loop / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: synthetic 13659-bus/4092-unit/36-period SCUC "
+                               f"LP relaxation + {args.triples or 1000} base flow triples",
+                   "rows": m, "cols": n, "nnz": nnz, "step": "16 HPR iterations + KKT check",
+                   "l2": "inputs larger than L2 (matrix stream > 1 GB/iteration)",
+                   "parallelism": f"replicas{ws}" if ws > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
+                     "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "bytes_per_launch": dom_b, "seconds_per_launch": dom_t,
+                     "peak_kind": peak_kind},
+        "iteration_roofline": {"bytes_per_iteration": bm["iter"], "achieved_gbs": it_gbs,
+                               "frac": it_gbs / peak},
+        "kernels": {"k_dual_s": k_dual, "k_primal_s": k_primal,
+                    "k_dual_gbs": bm["k_dual"] / k_dual / 1e9,
+                    "k_primal_gbs": bm["k_primal"] / k_primal / 1e9},
+        "gpu_launches": int(st.gpu_launches),
+        "setup": {"build_lp_s": t_build, "warmup_setup_s": st0.setup_seconds},
+    }
+    out["clocks"] = clk.summary()
+
+    if not args.no_e2e:
+        # public API from host buffers: upload + setup + solve to 1e-4 + copy back
+        lp_host = lpa.to_lp()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = hprlp.solve(lp_host, hprlp.SolverConfig(
+            tolerance=1e-4, ruiz=False, precision=Precision(args.precision),
+            max_iterations=args.e2e_max_iter))
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        h2d = 2 * (4 * (max(m, n) + 1)) + 2 * nnz * 12 + 8 * (m + 3 * n)
+        out["e2e"] = {"value": res.iterations / wall, "unit": "iterations/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * (2 * n + m),
+                      "time_to_tol_s": wall, "status": res.status.value,
+                      "iterations": res.iterations, "restarts": res.restarts,
+                      "objective": res.objective, "rel_kkt": res.kkt.max_rel,
+                      "loop_seconds": res.device_stats.get("loop_seconds")}
+    if rank == 0 and not args.no_cpu_baseline:
+        v, el = cpu_baseline_sample(lpa, st0.lam, st.sigma_final, args.precision)
+        out["cpu_baseline"] = {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
+                               "sample": f"oracle: {BLOCK} HPR iterations + 1 KKT check on the "
+                                         f"same LP ({el:.1f} s; scipy SpMV single-threaded; "
+                                         f"{os.cpu_count()} host cores available)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference algorithm on the host cores (oracle port — the reference
+    package itself is not on the GPU box): one step = one HPR iteration, a
+    KKT check every 16th step, on the same LP as the GPU arm."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import hpr_oracle as O
+    lpa, t_build = build_lp(args, "cuda:0" if _has_cuda() else None)
+    cfg = O.OracleConfig(tolerance=1e-4, ruiz=False, precision=args.precision)
+    p = O.Problem.from_lp(lpa)
+    t0 = time.perf_counter()
+    sc, w, lam, sigma = O.setup(p, cfg)
+    t_setup = time.perf_counter() - t0
+    m, n = p.a.shape
+    st = O.HprIterate(O.box(np.zeros(n), sc.work.lower, sc.work.upper), np.zeros(m), np.zeros(n),
+                      sigma, lam, cfg.dtype)
+
+    def step():
+        st.step(w)
+        if st.total % BLOCK == 0:
+            O.kkt(p, *sc.to_master(st.bx, st.by, st.bz))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iterations/s",
+           "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+           "data": "synthetic",
+           "config": {"workload": f"{args.config}: synthetic 13659-bus SCUC LP relaxation + "
+                                  f"{args.triples or 1000} base flow triples",
+                      "rows": m, "cols": n, "nnz": lpa.nnz,
+                      "step": "1 HPR iteration (KKT check every 16th)"},
+           "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
+                            "sample": f"{args.steps} iterations after {args.warmup} warm-up "
+                                      f"(oracle setup {t_setup:.1f} s untimed; scipy SpMV "
+                                      f"single-threaded, {os.cpu_count()} cores available)"},
+           "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def _has_cuda():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)

@@ -22,7 +22,7 @@ HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL 
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
            "hpr_destroy", "hpr_solve", "hpr_get_log", "hpr_matvec", "hpr_kkt_residual",
-           "hpr_power_method", "hpr_iterate")
+           "hpr_power_method", "hpr_iterate", "hpr_resume", "hpr_bench_kernel")
 
 _p = C.c_void_p
 
@@ -106,6 +106,8 @@ def load(path: str = LIB_PATH):
                                      C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32)]
     lib.hpr_iterate.argtypes = [_p, C.c_int32, C.c_double, C.c_double, C.c_int64] + [_p] * 12
+    lib.hpr_resume.argtypes = [_p, C.c_int64, C.c_double, C.POINTER(Stats)]
+    lib.hpr_bench_kernel.argtypes = [_p, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     _LIB = lib
     return lib
 

@@ -551,6 +551,14 @@ struct hpr_handle {
     long long launches = 0;
     std::vector<LogRec> h_log;
     cudaEvent_t ev[4];
+    // cached loop graph (kernel arguments are fixed per handle, so one
+    // instantiation serves every solve with the same block size and dtype)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    unsigned long long gcond = 0;
+    int g_B = 0, g_prec = -1;
+    long long g_per_block = 0;
+    int last_prec = -1;          // precision of the last solve (-1: none)
 };
 
 namespace {
@@ -880,6 +888,61 @@ void enqueue_iteration(hpr_handle* h, const Ptrs<T>& p, int j, bool check, cudaS
     }
 }
 
+template <typename T>
+void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
+    const int prec = sizeof(T) == 4 ? HPR_FP32 : HPR_FP64;
+    if (h->gexec && h->g_B == B && h->g_prec == prec) return;
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    h->gexec = nullptr;
+    h->graph = nullptr;
+    // WHILE(cond) { B fused iterations; master check; controller; copies }
+    CK(cudaGraphCreate(&h->graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, h->graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    const long long l0 = h->launches;
+    CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
+    enqueue_check<T>(h, p, 1, h->cap);
+    cudaGraph_t captured;
+    CK(cudaStreamEndCapture(h->cap, &captured));
+    h->g_per_block = h->launches - l0;
+    h->launches = l0;
+    CK(cudaGraphInstantiate(&h->gexec, h->graph, 0));
+    h->gcond = (unsigned long long)cond;
+    h->g_B = B;
+    h->g_prec = prec;
+}
+
+// Launch the cached loop graph from the current device state; returns the
+// device time of the loop (CUDA events on the handle's stream).
+double run_loop(hpr_handle* h) {
+    cudaStream_t s = h->stream;
+    unsigned long long cv = h->gcond;
+    CK(cudaMemcpyAsync(&h->ctrl->cond, &cv, sizeof(cv), cudaMemcpyHostToDevice, s));
+    const long long t_before = h->h_ctrl->total;
+    CK(cudaEventRecord(h->ev[2], s));
+    CK(cudaGraphLaunch(h->gexec, s));
+    CK(cudaEventRecord(h->ev[3], s));
+    unsigned long long zero = 0;
+    CK(cudaMemcpyAsync(&h->ctrl->cond, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    h->launches += h->g_per_block * ((h->h_ctrl->total - t_before) / h->g_B);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+    return ms * 1e-3;
+}
+
 void read_ctrl(hpr_handle* h) {
     CK(cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -995,47 +1058,11 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
             int one = 1;
             CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
         }
-        // graph: WHILE(cond) { B fused iterations; check; controller; copies }
-        cudaGraph_t g;
-        CK(cudaGraphCreate(&g, 0));
-        cudaGraphConditionalHandle cond;
-        CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
-        cudaGraphNodeParams np = {};
-        np.type = cudaGraphNodeTypeConditional;
-        np.conditional.handle = cond;
-        np.conditional.type = cudaGraphCondTypeWhile;
-        np.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
-        cudaGraph_t body = np.conditional.phGraph_out[0];
-        unsigned long long cv = (unsigned long long)cond;
-        CK(cudaMemcpyAsync(&h->ctrl->cond, &cv, sizeof(cv), cudaMemcpyHostToDevice, s));
-        const long long l0 = h->launches;
-        CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
-                                         cudaStreamCaptureModeThreadLocal));
-        for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
-        enqueue_check<T>(h, p, 1, h->cap);
-        cudaGraph_t captured;
-        CK(cudaStreamEndCapture(h->cap, &captured));
-        const long long per_block = h->launches - l0;
-        h->launches = l0;
-        cudaGraphExec_t ex;
-        CK(cudaGraphInstantiate(&ex, g, 0));
-        CK(cudaEventRecord(h->ev[2], s));
-        CK(cudaGraphLaunch(ex, s));
-        CK(cudaEventRecord(h->ev[3], s));
-        read_ctrl(h);
-        cudaGraphExecDestroy(ex);
-        cudaGraphDestroy(g);
-        unsigned long long zero = 0;
-        CK(cudaMemcpyAsync(&h->ctrl->cond, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+        ensure_graph<T>(h, p, B);
+        st->loop_seconds = run_loop(h);
         status = h->h_ctrl->status;
         iterations = h->h_ctrl->total;
         if (status == HPR_ITERATION_LIMIT) iterations = prm->max_iterations;
-        h->launches += per_block * (h->h_ctrl->total / B);
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
-        st->loop_seconds = ms * 1e-3;
     } else {
         st->loop_seconds = 0.0;
     }
@@ -1056,6 +1083,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     st->power_iterations = pits;
     st->power_converged = pconv;
     st->checks = hc.checks;
+    h->last_prec = fp32 ? HPR_FP32 : HPR_FP64;
     if (xo) CK(cudaMemcpyAsync(xo, h->BXm, sizeof(double) * n, cudaMemcpyDefault, s));
     if (yo) CK(cudaMemcpyAsync(yo, h->BYm, sizeof(double) * m, cudaMemcpyDefault, s));
     if (zo) CK(cudaMemcpyAsync(zo, h->BZm, sizeof(double) * n, cudaMemcpyDefault, s));
@@ -1217,6 +1245,8 @@ void hpr_destroy(hpr_handle* h) {
     if (h->h_scal) cudaFreeHost(h->h_scal);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->graph) cudaGraphDestroy(h->graph);
     if (h->cap) cudaStreamDestroy(h->cap);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -1403,6 +1433,70 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     get(h->BY, bar_y, m, nullptr);
     get(h->BZ, bar_z, n, nullptr);
     CK(cudaStreamSynchronize(s));
+    API_END
+}
+
+int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* st) {
+    API_BEGIN
+    if (!h || !st) fail(HPR_ERR_INVALID, "NULL argument");
+    if (h->last_prec < 0 || !h->gexec) fail(HPR_ERR_INVALID, "hpr_resume needs a prior looping solve");
+    CK(cudaSetDevice(h->dev));
+    std::memset(st, 0, sizeof(*st));
+    h->launches = 0;
+    read_ctrl(h);
+    Ctrl c = *h->h_ctrl;
+    c.max_iter = c.total + more_iterations;
+    c.status = more_iterations >= c.B ? -1 : HPR_ITERATION_LIMIT;
+    c.has_deadline = 0;
+    if (tolerance > 0) c.tol = tolerance;
+    c.cond = 0;
+    CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+    *h->h_ctrl = c;
+    st->loop_seconds = c.status == -1 ? run_loop(h) : 0.0;
+    const Ctrl& hc = *h->h_ctrl;
+    st->status = hc.status;
+    st->precision_used = h->last_prec;
+    st->iterations = hc.total - (c.max_iter - more_iterations);
+    st->restarts = hc.restarts;
+    st->sigma_final = hc.sigma;
+    st->lam = hc.lam;
+    std::memcpy(&st->kkt, hc.best, sizeof(hpr_kkt));
+    st->objective = hc.best[6];
+    st->checks = hc.checks;
+    st->gpu_launches = h->launches;
+    API_END
+}
+
+int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds_per_launch) {
+    API_BEGIN
+    if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
+    if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
+    CK(cudaSetDevice(h->dev));
+    cudaStream_t s = h->stream;
+    auto body = [&](auto tag) {
+        using T = decltype(tag);
+        Ptrs<T> p = ptrs<T>(h, sizeof(T) == 4);
+        if (which == 0) {
+            EpiDual<T, false> e2{h->ctrl, 0, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
+            launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s);
+        } else {
+            EpiPrimal<T, false> e1{h->ctrl, 0, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
+                                   p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
+            launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s);
+        }
+    };
+    auto run = [&]() {
+        if (h->last_prec == HPR_FP32) body(float(0));
+        else body(double(0));
+    };
+    run();  // warm
+    CK(cudaEventRecord(h->ev[0], s));
+    for (int r = 0; r < reps; ++r) run();
+    CK(cudaEventRecord(h->ev[1], s));
+    CK(cudaEventSynchronize(h->ev[1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    *seconds_per_launch = ms * 1e-3 / reps;
     API_END
 }
 

@@ -300,6 +300,21 @@ class Engine:
                                           *[_capi.ptr(o) for o in outs]))
         return outs
 
+    def resume(self, more_iterations, tolerance=0.0) -> _capi.Stats:
+        """Continue the last solve's device state (benchmark support)."""
+        st = _capi.Stats()
+        _capi.check(self._lib.hpr_resume(self._h, int(more_iterations), float(tolerance),
+                                         _capi.C.byref(st)))
+        return st
+
+    def bench_kernel(self, which: int, reps: int = 20) -> float:
+        """Average device seconds of one fused iteration kernel
+        (0: A x~ + dual update, 1: A^T y + primal update)."""
+        sec = _capi.C.c_double()
+        _capi.check(self._lib.hpr_bench_kernel(self._h, int(which), int(reps),
+                                               _capi.C.byref(sec)))
+        return sec.value
+
     def solve_raw(self, config, start=None, time_elapsed=0.0):
         """One ``_solve_once`` on the device; returns (x, y, z, Stats, log)."""
         cfg = config

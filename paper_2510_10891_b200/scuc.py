@@ -70,7 +70,20 @@ def _dc_flows(n_b, fb, tb, react, injections, ref=0):
     import scipy.sparse.linalg as spla
     lap, keep = _bus_laplacian_reduced(n_b, fb, tb, react, ref)
     theta = np.zeros((n_b, injections.shape[1]))
-    theta[keep] = spla.splu(lap).solve(np.ascontiguousarray(injections[keep]))
+    rhs = np.ascontiguousarray(injections[keep])
+    if n_b <= 2000:
+        theta[keep] = spla.splu(lap).solve(rhs)
+    else:
+        # random chords make sparse LU fill in; the reduced Laplacian is SPD,
+        # so Jacobi-preconditioned CG is cheap (limits are rounded to 1e-3 MW)
+        lap = lap.tocsr()
+        dinv = 1.0 / lap.diagonal()
+        pre = spla.LinearOperator(lap.shape, matvec=lambda v: dinv * v)
+        for k in range(rhs.shape[1]):
+            sol, info = spla.cg(lap, rhs[:, k], rtol=1e-13, atol=0.0, maxiter=20000, M=pre)
+            if info != 0:
+                raise RuntimeError("DC-flow CG did not converge")
+            theta[keep, k] = sol
     return (theta[fb] - theta[tb]) / react[:, None]
 
 
@@ -637,7 +650,7 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
     c_all = np.concatenate(rows.c)
     v_all = np.concatenate(rows.v)
     m = rows.n
-    order = np.lexsort((c_all, r_all))
+    order = np.argsort(r_all * np.int64(n) + c_all, kind="stable")
     r_all, c_all, v_all = r_all[order], c_all[order], v_all[order]
     dup = np.flatnonzero((r_all[1:] == r_all[:-1]) & (c_all[1:] == c_all[:-1]))
     if dup.size:
