@@ -84,26 +84,61 @@ __global__ void k_row_absmax(const int* ptr, const double* vals, int rows, doubl
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src),
 // which scipy's abs(A).sum(axis) reaches through np.add.reduceat:
-// segment sum = a[0] + pairwise(a[1:]).
-__device__ double np_pairwise_abs(const double* a, int n) {
+// segment sum = a[0] + pairwise(a[1:]).  Leaves of <= 128 elements use 8
+// strided accumulators; larger ranges split at a multiple of 8 below n/2.
+// The recursion is unrolled onto a small explicit stack (the default device
+// stack is too small for deep recursion on ~20K-entry rows).
+__device__ double np_pairwise_leaf(const double* a, int n) {
     if (n < 8) {
         double r = 0.0;
         for (int i = 0; i < n; ++i) r += fabs(a[i]);
         return r;
     }
-    if (n <= 128) {
-        double r[8];
-        for (int k = 0; k < 8; ++k) r[k] = fabs(a[k]);
-        int i = 8;
-        for (; i < n - (n % 8); i += 8)
-            for (int k = 0; k < 8; ++k) r[k] += fabs(a[i + k]);
-        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        for (; i < n; ++i) res += fabs(a[i]);
-        return res;
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = fabs(a[k]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int k = 0; k < 8; ++k) r[k] += fabs(a[i + k]);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += fabs(a[i]);
+    return res;
+}
+
+__device__ double np_pairwise_abs(const double* a, int n) {
+    int off[32], len[32], state[32];
+    double left[32];
+    int sp = 0;
+    off[0] = 0;
+    len[0] = n;
+    state[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        if (len[sp] <= 128) {
+            ret = np_pairwise_leaf(a + off[sp], len[sp]);
+            --sp;
+            continue;
+        }
+        int n2 = len[sp] / 2;
+        n2 -= n2 % 8;
+        if (state[sp] == 0) {
+            state[sp] = 1;
+            off[sp + 1] = off[sp];
+            len[sp + 1] = n2;
+            state[sp + 1] = 0;
+            ++sp;
+        } else if (state[sp] == 1) {
+            left[sp] = ret;
+            state[sp] = 2;
+            off[sp + 1] = off[sp] + n2;
+            len[sp + 1] = len[sp] - n2;
+            state[sp + 1] = 0;
+            ++sp;
+        } else {
+            ret = left[sp] + ret;
+            --sp;
+        }
     }
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    return np_pairwise_abs(a, n2) + np_pairwise_abs(a + n2, n - n2);
+    return ret;
 }
 
 __global__ void k_row_abssum(const int* ptr, const double* vals, int rows, double* out) {
