@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, LIB_NAME)
 
 HPR_OPTIMAL, HPR_ITERATION_LIMIT, HPR_TIME_LIMIT, HPR_NUMERICAL_FAILURE = 0, 1, 2, 3
 HPR_FP64, HPR_FP32 = 0, 1
+HPR_FLAG_NO_REORDER = 1
 HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
@@ -37,7 +38,7 @@ class Problem(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("stream", _p), ("workspace", _p),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32)]
 
 
 class Params(C.Structure):

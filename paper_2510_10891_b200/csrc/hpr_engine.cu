@@ -594,6 +594,10 @@ struct hpr_handle {
     int g_B = 0, g_prec = -1;
     long long g_per_block = 0;
     int last_prec = -1;          // precision of the last solve (-1: none)
+    // locality ordering (new -> old); identity when reorder is off
+    bool reordered = false;
+    int *rperm = nullptr, *cperm = nullptr;
+    double* stage = nullptr;     // max(m, n) staging for permuted I/O
 };
 
 namespace {
@@ -604,8 +608,27 @@ struct Layout {
     size_t bytes;
 };
 
+// Upper bounds on the tile schedule of a CSR with `rows` rows and `nnz`
+// nonzeros, independent of the row order (so the workspace can be sized
+// before the locality ordering is computed).  A stream tile closes on a
+// full row count, on nnz overflow (two consecutive tiles then hold more than
+// TILE_NNZ), before a long row, or at the end.
+struct TileBound {
+    size_t tiles, longs;
+};
+TileBound tile_bound(long long rows, long long nnz) {
+    const long long nlong = std::min<long long>(rows, nnz / (TILE_NNZ + 1));
+    const long long t = 2 * (nnz / TILE_NNZ + 1) + rows / TILE_ROWS + 1 + 2 * nlong +
+                        (nnz / CHUNK_NNZ + 1) + nlong + 2;
+    return {(size_t)t, (size_t)std::max<long long>(nlong, 1)};
+}
+
 // Carve every device array from one block; base == nullptr only measures.
-size_t carve(hpr_handle* h, char* base, const Plan& pa, const Plan& pt) {
+size_t carve(hpr_handle* h, char* base) {
+    const TileBound ba = tile_bound(h->m, h->nnz), bt = tile_bound(h->n, h->nnz);
+    struct {
+        size_t tiles, longs;
+    } pa_{ba.tiles, ba.longs}, pt_{bt.tiles, bt.longs};
     Carver cv;
     cv.base = base;
     const size_t m = h->m, n = h->n, nnz = h->nnz;
@@ -619,14 +642,14 @@ size_t carve(hpr_handle* h, char* base, const Plan& pa, const Plan& pt) {
     h->AT.mval = cv.take<double>(nnz);
     h->AT.w64 = cv.take<double>(nnz);
     h->AT.w32 = cv.take<float>(nnz);
-    h->A.tiles = cv.take<int4>(pa.tiles.size());
-    h->A.longs = cv.take<int4>(pa.longs.size());
-    h->A.counters = cv.take<int>(pa.longs.size());
-    h->A.tpart = cv.take<double>(pa.tiles.size());
-    h->AT.tiles = cv.take<int4>(pt.tiles.size());
-    h->AT.longs = cv.take<int4>(pt.longs.size());
-    h->AT.counters = cv.take<int>(pt.longs.size());
-    h->AT.tpart = cv.take<double>(pt.tiles.size());
+    h->A.tiles = cv.take<int4>(pa_.tiles);
+    h->A.longs = cv.take<int4>(pa_.longs);
+    h->A.counters = cv.take<int>(pa_.longs);
+    h->A.tpart = cv.take<double>(pa_.tiles);
+    h->AT.tiles = cv.take<int4>(pt_.tiles);
+    h->AT.longs = cv.take<int4>(pt_.longs);
+    h->AT.counters = cv.take<int>(pt_.longs);
+    h->AT.tpart = cv.take<double>(pt_.tiles);
     h->rhs_m = cv.take<double>(m);
     h->cost_m = cv.take<double>(n);
     h->lo_m = cv.take<double>(n);
@@ -659,14 +682,81 @@ size_t carve(hpr_handle* h, char* base, const Plan& pa, const Plan& pt) {
     h->BXm = cv.take<double>(n);
     h->BZm = cv.take<double>(n);
     h->BYm = cv.take<double>(m);
-    const size_t nsa = pa.tiles.size() + pa.longs.size(), nst = pt.tiles.size() + pt.longs.size();
+    const size_t nsa = pa_.tiles + pa_.longs, nst = pt_.tiles + pt_.longs;
     h->rowpart = cv.take<double>(KR * nsa);
     h->colpart = cv.take<double>(KC * std::max(nst, nsa));
     h->red = cv.take<double>(RED_BLOCKS + 64);
     h->pw = cv.take<double>(m + n);
+    h->rperm = cv.take<int>(m);
+    h->cperm = cv.take<int>(n);
+    h->stage = cv.take<double>(std::max(m, n));
     h->ctrl = cv.take<Ctrl>(1);
     h->d_dev = cv.take<unsigned long long>(2);
     return cv.off + 256;
+}
+
+// Locality ordering (SURVEY.md §7 hard part 5).  The reference lays
+// variables out [g, t] (formulation.py:53-69), so a period-t flow row
+// gathers x at stride T.  Columns are regrouped by the first long row
+// (> LONG_ROW nonzeros) that touches them — for SCUC the balance row of
+// their period — and rows (equalities and inequalities separately, so the
+// n_eq prefix is preserved) by their smallest new column.  Entry order
+// inside every row of A and A^T stays the original one, so every row sum
+// keeps the reference's summation order; only the labels move.
+constexpr int LONG_ROW = 256;
+
+void compute_order(int m, int n, int n_eq, const std::vector<int32_t>& ptr,
+                   const std::vector<int32_t>& idx, std::vector<int32_t>& rperm,
+                   std::vector<int32_t>& cperm) {
+    const int INF = 0x7fffffff;
+    std::vector<int32_t> ckey(n, INF);
+    for (int i = 0; i < m; ++i)
+        if (ptr[i + 1] - ptr[i] > LONG_ROW)
+            for (int e = ptr[i]; e < ptr[i + 1]; ++e)
+                if (ckey[idx[e]] == INF) ckey[idx[e]] = i;
+    cperm.resize(n);
+    for (int j = 0; j < n; ++j) cperm[j] = j;
+    std::stable_sort(cperm.begin(), cperm.end(),
+                     [&](int a, int b) { return ckey[a] < ckey[b]; });
+    std::vector<int32_t> cinv(n);
+    for (int k = 0; k < n; ++k) cinv[cperm[k]] = k;
+    std::vector<int32_t> rkey(m, INF);
+    for (int i = 0; i < m; ++i)
+        for (int e = ptr[i]; e < ptr[i + 1]; ++e) rkey[i] = std::min(rkey[i], cinv[idx[e]]);
+    rperm.resize(m);
+    for (int i = 0; i < m; ++i) rperm[i] = i;
+    auto by = [&](int a, int b) { return rkey[a] < rkey[b]; };
+    std::stable_sort(rperm.begin(), rperm.begin() + n_eq, by);
+    std::stable_sort(rperm.begin() + n_eq, rperm.end(), by);
+}
+
+// relabel a CSR: new row r' = old row perm_rows[r'], columns through inv_cols
+void permute_csr(int rows, const std::vector<int32_t>& ptr, const std::vector<int32_t>& idx,
+                 const std::vector<double>& val, const std::vector<int32_t>& perm_rows,
+                 const std::vector<int32_t>& inv_cols, std::vector<int32_t>& nptr,
+                 std::vector<int32_t>& nidx, std::vector<double>& nval) {
+    nptr.assign(rows + 1, 0);
+    for (int r = 0; r < rows; ++r) nptr[r + 1] = nptr[r] + (ptr[perm_rows[r] + 1] - ptr[perm_rows[r]]);
+    nidx.resize(idx.size());
+    nval.resize(val.size());
+    for (int r = 0; r < rows; ++r) {
+        const int o = perm_rows[r];
+        int q = nptr[r];
+        for (int e = ptr[o]; e < ptr[o + 1]; ++e, ++q) {
+            nidx[q] = inv_cols[idx[e]];
+            nval[q] = val[e];
+        }
+    }
+}
+
+__global__ void k_gather(double* dst, const double* src, const int* perm, int len) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) dst[i] = src[perm[i]];
+}
+
+__global__ void k_scatter(double* dst, const double* src, const int* perm, int len) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) dst[perm[i]] = src[i];
 }
 
 void host_transpose(int m, int n, const int32_t* ptr, const int32_t* idx, const double* val,
@@ -703,6 +793,28 @@ std::vector<T> to_host(const T* p, size_t count) {
 }
 
 inline int nblk(long long n, int tpb = TPB) { return (int)std::max<long long>(1, (n + tpb - 1) / tpb); }
+
+// caller vector (original order, host or device) -> device vector (engine order)
+void put_vec(hpr_handle* h, double* dst, const double* src, int len, bool rows) {
+    if (!h->reordered) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(double) * len, cudaMemcpyDefault, h->stream));
+        return;
+    }
+    CK(cudaMemcpyAsync(h->stage, src, sizeof(double) * len, cudaMemcpyDefault, h->stream));
+    k_gather<<<nblk(len), TPB, 0, h->stream>>>(dst, h->stage, rows ? h->rperm : h->cperm, len);
+    CKL();
+}
+
+// device vector (engine order) -> caller vector (original order, host or device)
+void get_vec(hpr_handle* h, double* dst, const double* src, int len, bool rows) {
+    if (!h->reordered) {
+        CK(cudaMemcpyAsync(dst, src, sizeof(double) * len, cudaMemcpyDefault, h->stream));
+        return;
+    }
+    k_scatter<<<nblk(len), TPB, 0, h->stream>>>(h->stage, src, rows ? h->rperm : h->cperm, len);
+    CKL();
+    CK(cudaMemcpyAsync(dst, h->stage, sizeof(double) * len, cudaMemcpyDefault, h->stream));
+}
 
 void validate(const hpr_problem* p) {
     if (!p) fail(HPR_ERR_INVALID, "problem is NULL");
@@ -746,8 +858,7 @@ double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, 
     int used = 0;
     auto load_start = [&]() {
         if (used >= start_count) fail(HPR_ERR_POWER_NULL, "power_method exhausted start vectors");
-        CK(cudaMemcpyAsync(v, start + (size_t)used * h->m, sizeof(double) * h->m, cudaMemcpyDefault,
-                           h->stream));
+        put_vec(h, v, start + (size_t)used * h->m, h->m, true);
         ++used;
         const double nv = std::sqrt(dev_sumsq(h, v, h->m, 0));
         k_div<<<nblk(h->m), TPB, 0, h->stream>>>(v, h->m, nv);
@@ -1022,9 +1133,9 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     // device-resident warm start (master space)
     const double *dx0 = nullptr, *dy0 = nullptr, *dz0 = nullptr;
     if (x0 && y0 && z0) {
-        CK(cudaMemcpyAsync(h->BXm, x0, sizeof(double) * n, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(h->BYm, y0, sizeof(double) * m, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(h->BZm, z0, sizeof(double) * n, cudaMemcpyDefault, s));
+        put_vec(h, h->BXm, x0, n, false);
+        put_vec(h, h->BYm, y0, m, true);
+        put_vec(h, h->BZm, z0, n, false);
         dx0 = h->BXm;
         dy0 = h->BYm;
         dz0 = h->BZm;
@@ -1119,9 +1230,9 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     st->power_converged = pconv;
     st->checks = hc.checks;
     h->last_prec = fp32 ? HPR_FP32 : HPR_FP64;
-    if (xo) CK(cudaMemcpyAsync(xo, h->BXm, sizeof(double) * n, cudaMemcpyDefault, s));
-    if (yo) CK(cudaMemcpyAsync(yo, h->BYm, sizeof(double) * m, cudaMemcpyDefault, s));
-    if (zo) CK(cudaMemcpyAsync(zo, h->BZm, sizeof(double) * n, cudaMemcpyDefault, s));
+    if (xo) get_vec(h, xo, h->BXm, n, false);
+    if (yo) get_vec(h, yo, h->BYm, m, true);
+    if (zo) get_vec(h, zo, h->BZm, n, false);
     if (st->n_log) {
         h->h_log.resize(st->n_log);
         CK(cudaMemcpyAsync(h->h_log.data(), h->log, sizeof(LogRec) * st->n_log,
@@ -1161,21 +1272,12 @@ const char* hpr_last_error(void) { return g_err.c_str(); }
 int hpr_workspace_bytes(const hpr_problem* p, size_t* bytes) {
     API_BEGIN
     validate(p);
-    std::vector<int32_t> ptr = to_host(p->indptr, (size_t)p->m + 1);
-    std::vector<int32_t> tptr;
-    if (p->t_indptr) {
-        tptr = to_host(p->t_indptr, (size_t)p->n + 1);
-    } else {
-        std::vector<int32_t> idx = to_host(p->indices, (size_t)p->nnz);
-        tptr.assign(p->n + 1, 0);
-        for (auto c : idx) tptr[c + 1]++;
-        for (int j = 0; j < p->n; ++j) tptr[j + 1] += tptr[j];
-    }
+    if (!bytes) fail(HPR_ERR_INVALID, "bytes is NULL");
     hpr_handle tmp;
     tmp.m = p->m;
     tmp.n = p->n;
     tmp.nnz = p->nnz;
-    *bytes = carve(&tmp, nullptr, plan_for(ptr.data(), p->m), plan_for(tptr.data(), p->n));
+    *bytes = carve(&tmp, nullptr);
     API_END
 }
 
@@ -1209,8 +1311,33 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         } else {
             host_transpose(p->m, p->n, ptr.data(), idx.data(), val.data(), tptr, tidx, tval);
         }
+        std::vector<int32_t> rperm, cperm;
+        const bool reorder = !(opt && (opt->flags & HPR_FLAG_NO_REORDER));
+        if (reorder) {
+            compute_order(p->m, p->n, p->n_eq, ptr, idx, rperm, cperm);
+            std::vector<int32_t> rinv(p->m), cinv(p->n);
+            for (int i = 0; i < p->m; ++i) rinv[rperm[i]] = i;
+            for (int j = 0; j < p->n; ++j) cinv[cperm[j]] = j;
+            std::vector<int32_t> a, b;
+            std::vector<double> c;
+            permute_csr(p->m, ptr, idx, val, rperm, cinv, a, b, c);
+            ptr.swap(a);
+            idx.swap(b);
+            val.swap(c);
+            permute_csr(p->n, tptr, tidx, tval, cperm, rinv, a, b, c);
+            tptr.swap(a);
+            tidx.swap(b);
+            tval.swap(c);
+            h->reordered = true;
+        }
         Plan pa = plan_for(ptr.data(), p->m), pt = plan_for(tptr.data(), p->n);
-        const size_t need = carve(h, nullptr, pa, pt);
+        {
+            const TileBound ba = tile_bound(p->m, p->nnz), bt = tile_bound(p->n, p->nnz);
+            if (pa.tiles.size() > ba.tiles || pt.tiles.size() > bt.tiles ||
+                pa.longs.size() > ba.longs || pt.longs.size() > bt.longs)
+                fail(HPR_ERR_INVALID, "internal: tile bound violated");
+        }
+        const size_t need = carve(h, nullptr);
         if (opt && opt->workspace) {
             if (opt->workspace_bytes < need) fail(HPR_ERR_NOMEM, "workspace too small");
             h->ws = opt->workspace;
@@ -1220,7 +1347,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             h->own_ws = true;
             h->ws_bytes = need;
         }
-        carve(h, (char*)h->ws, pa, pt);
+        carve(h, (char*)h->ws);
         if (opt && opt->stream) {
             h->stream = (cudaStream_t)opt->stream;
         } else {
@@ -1252,10 +1379,14 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         CK(cudaMemcpyAsync(h->AT.longs, pt.longs.data(), sizeof(int4) * pt.longs.size(), cudaMemcpyHostToDevice, s));
         if (!pa.longs.empty()) CK(cudaMemsetAsync(h->A.counters, 0, sizeof(int) * pa.longs.size(), s));
         if (!pt.longs.empty()) CK(cudaMemsetAsync(h->AT.counters, 0, sizeof(int) * pt.longs.size(), s));
-        CK(cudaMemcpyAsync(h->rhs_m, p->rhs, sizeof(double) * p->m, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(h->cost_m, p->cost, sizeof(double) * p->n, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(h->lo_m, p->lower, sizeof(double) * p->n, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(h->up_m, p->upper, sizeof(double) * p->n, cudaMemcpyDefault, s));
+        if (h->reordered) {
+            CK(cudaMemcpyAsync(h->rperm, rperm.data(), sizeof(int) * p->m, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(h->cperm, cperm.data(), sizeof(int) * p->n, cudaMemcpyHostToDevice, s));
+        }
+        put_vec(h, h->rhs_m, p->rhs, p->m, true);
+        put_vec(h, h->cost_m, p->cost, p->n, false);
+        put_vec(h, h->lo_m, p->lower, p->n, false);
+        put_vec(h, h->up_m, p->upper, p->n, false);
         CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
         CK(cudaStreamSynchronize(s));
         *out = h;
@@ -1330,10 +1461,10 @@ int hpr_matvec(hpr_handle* h, int32_t transpose, const double* in, double* out) 
     const DevCsr& M = transpose ? h->AT : h->A;
     const int nin = transpose ? h->m : h->n, nout = transpose ? h->n : h->m;
     double* xin = transpose ? h->YM : h->XM;   // master scratch of the input length
-    CK(cudaMemcpyAsync(xin, in, sizeof(double) * nin, cudaMemcpyDefault, h->stream));
+    put_vec(h, xin, in, nin, transpose != 0);
     EpiStore<double> st{h->pw, nullptr};       // pw holds m + n doubles
     launch_spmv(h, M, (const double*)M.mval, (const double*)xin, st, h->stream);
-    CK(cudaMemcpyAsync(out, h->pw, sizeof(double) * nout, cudaMemcpyDefault, h->stream));
+    get_vec(h, out, h->pw, nout, transpose == 0);
     CK(cudaStreamSynchronize(h->stream));
     API_END
 }
@@ -1344,9 +1475,9 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     if (!h || !x || !y || !z || !out) fail(HPR_ERR_INVALID, "NULL argument");
     CK(cudaSetDevice(h->dev));
     cudaStream_t s = h->stream;
-    CK(cudaMemcpyAsync(h->XM, x, sizeof(double) * h->n, cudaMemcpyDefault, s));
-    CK(cudaMemcpyAsync(h->YM, y, sizeof(double) * h->m, cudaMemcpyDefault, s));
-    CK(cudaMemcpyAsync(h->ZM, z, sizeof(double) * h->n, cudaMemcpyDefault, s));
+    put_vec(h, h->XM, x, h->n, false);
+    put_vec(h, h->YM, y, h->m, true);
+    put_vec(h, h->ZM, z, h->n, false);
     // bar/anchor terms are irrelevant here: point them at zeroed work buffers
     CK(cudaMemsetAsync(h->BX, 0, sizeof(double) * h->n, s));
     CK(cudaMemsetAsync(h->BZ, 0, sizeof(double) * h->n, s));
@@ -1417,35 +1548,35 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     c.b_scale = 1.0;
     c.c_scale = 1.0;
     CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
-    // stage the six state vectors through the master scratch, cast to the work dtype
-    auto put = [&](const double* src, void* dst, int len, double* scratch) {
+    // stage the six state vectors (engine order), cast to the work dtype
+    auto put = [&](const double* src, void* dst, int len, double* scratch, bool rows) {
+        put_vec(h, scratch, src, len, rows);
         if (fp32) {
-            CK(cudaMemcpyAsync(scratch, src, sizeof(double) * len, cudaMemcpyDefault, s));
             k_cast_f32<<<nblk(len), TPB, 0, s>>>(scratch, (float*)dst, len);
             CKL();
         } else {
-            CK(cudaMemcpyAsync(dst, src, sizeof(double) * len, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(dst, scratch, sizeof(double) * len, cudaMemcpyDeviceToDevice, s));
         }
     };
-    put(x, h->X, n, h->XM);
-    put(z, h->Z, n, h->ZM);
-    put(ax, h->AXv, n, h->BXm);
-    put(az, h->AZv, n, h->BZm);
-    put(y, h->Y, m, h->YM);
-    put(ay, h->AYv, m, h->BYm);
-    auto get = [&](const void* src, double* dst, int len, double* scratch) {
+    put(x, h->X, n, h->XM, false);
+    put(z, h->Z, n, h->ZM, false);
+    put(ax, h->AXv, n, h->BXm, false);
+    put(az, h->AZv, n, h->BZm, false);
+    put(y, h->Y, m, h->YM, true);
+    put(ay, h->AYv, m, h->BYm, true);
+    auto get = [&](const void* src, double* dst, int len, double* scratch, bool rows) {
         if (!dst) return;
         if (fp32) {
             std::vector<float> tmp(len);
             CK(cudaMemcpyAsync(tmp.data(), src, sizeof(float) * len, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             std::vector<double> d(tmp.begin(), tmp.end());
-            CK(cudaMemcpyAsync(dst, d.data(), sizeof(double) * len, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(scratch, d.data(), sizeof(double) * len, cudaMemcpyHostToDevice, s));
             CK(cudaStreamSynchronize(s));
+            get_vec(h, dst, scratch, len, rows);
         } else {
-            CK(cudaMemcpyAsync(dst, src, sizeof(double) * len, cudaMemcpyDefault, s));
+            get_vec(h, dst, (const double*)src, len, rows);
         }
-        (void)scratch;
     };
     if (fp32) {
         k_cast_f32<<<nblk(h->nnz), TPB, 0, s>>>(h->A.w64, h->A.w32, h->nnz);
@@ -1461,12 +1592,12 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
         Ptrs<double> p = ptrs<double>(h, false);
         enqueue_iteration<double>(h, p, 0, true, s);
     }
-    get(h->X, x_out, n, nullptr);
-    get(h->Y, y_out, m, nullptr);
-    get(h->Z, z_out, n, nullptr);
-    get(h->BX, bar_x, n, nullptr);
-    get(h->BY, bar_y, m, nullptr);
-    get(h->BZ, bar_z, n, nullptr);
+    get(h->X, x_out, n, h->XM, false);
+    get(h->Y, y_out, m, h->YM, true);
+    get(h->Z, z_out, n, h->ZM, false);
+    get(h->BX, bar_x, n, h->XM, false);
+    get(h->BY, bar_y, m, h->YM, true);
+    get(h->BZ, bar_z, n, h->ZM, false);
     CK(cudaStreamSynchronize(s));
     API_END
 }

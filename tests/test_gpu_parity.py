@@ -189,3 +189,25 @@ def test_log_every_iteration_rate_log(H):
     b = np.array(o.rate_log)
     np.testing.assert_array_equal(a[:, :2], b[:, :2])
     np.testing.assert_allclose(a[:, 2], b[:, 2], rtol=1e-8, atol=1e-14)
+
+
+def test_locality_reorder_is_transparent(H):
+    """The engine's period-major relabelling must not change results."""
+    from paper_2510_10891_b200 import scuc
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7)
+    lpa = scuc.build_relaxation(doc, scuc.sample_monitored(doc, 300, 7))
+    lp = lpa.to_lp()
+    cfg = H.SolverConfig(tolerance=1e-4, ruiz=True)
+    outs = []
+    for reorder in (False, True):
+        eng = H.Engine(lp, reorder=reorder)
+        x, y, z, st, _ = eng.solve_raw(cfg)
+        outs.append((x, y, z, st.iterations, st.restarts, st.lam))
+        rng = np.random.default_rng(1)
+        v = rng.standard_normal(lpa.shape[1])
+        np.testing.assert_allclose(eng.matvec(v), lpa.csr() @ v, rtol=1e-13, atol=1e-12)
+        eng.close()
+    a, b = outs
+    assert a[3:5] == b[3:5]
+    assert a[5] == pytest.approx(b[5], rel=1e-13)
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-7, atol=1e-9)
