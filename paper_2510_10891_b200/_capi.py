@@ -85,11 +85,13 @@ class HprError(RuntimeError):
 _LIB = None
 
 
-def load(path: str = LIB_PATH):
-    """Load the shared library and declare signatures (no device needed)."""
+def load(path: str | None = None):
+    """Load the shared library and declare signatures (no device needed).
+    HPR_LIB overrides the in-tree path (kernel-variant experiments)."""
     global _LIB
     if _LIB is not None:
         return _LIB
+    path = path or os.environ.get("HPR_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: run __graft_entry__.build() (or make) first")
     lib = C.CDLL(path)

@@ -15,9 +15,9 @@ namespace hpr {
 
 constexpr int TPB = 256;          // threads per CTA for every tiled kernel
 constexpr int TILE_NNZ = 2048;    // nonzeros staged per stream tile (16 KB FP64 products)
-constexpr int TILE_ROWS = 1024;   // rows per stream tile
+constexpr int TILE_ROWS = TPB;    // rows per stream tile (one epilogue row per thread)
 constexpr int ITEMS = TILE_NNZ / TPB;
-constexpr int CHUNK_NNZ = 4096;   // nonzeros per CTA on a long (split) row
+constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row (one pipeline stage)
 constexpr int MAX_B = 64;         // largest check_every the fused loop body supports
 
 // quantities accumulated by the two master-space check kernels
@@ -77,7 +77,7 @@ struct Csr {
     const int* indptr;
     const int* indices;
     const T* vals;
-    const int4* tiles;       // {r0, r1, lanes, -1} stream tile | {row, e0, e1, long_idx} chunk
+    const int4* tiles;       // {r0, -(r1+1), p0, p1} stream tile | {row, e0, e1, long_idx} chunk
     int ntiles;
     const int4* longs;       // {row, first_tile, nchunks, 0}
     int nlong;

@@ -34,6 +34,7 @@
 
 #include "hpr_common.cuh"
 #include "hpr_spmv.cuh"
+#include "hpr_spmv_pipe.cuh"
 #include "../../include/hprlp_b200.h"
 
 using namespace hpr;
@@ -509,10 +510,7 @@ Plan build_tiles(const int32_t* ptr, int rows) {
             nz += l;
             ++r;
         }
-        const int R = r - r0;
-        int L = 1;
-        while (L < 32 && (L * 2) * R <= TPB && (long long)L * R < nz) L *= 2;
-        p.tiles.push_back(make_int4(r0, r, L, -1));
+        p.tiles.push_back(make_int4(r0, -(r + 1), ptr[r0], ptr[r]));
     }
     return p;
 }
@@ -524,7 +522,7 @@ struct Carver {
     T* take(size_t count) {
         off = (off + 255) & ~size_t(255);
         T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
-        off += sizeof(T) * std::max<size_t>(count, 1);
+        off += sizeof(T) * std::max<size_t>(count, 1) + 64;   // tail pad: 16-byte bulk-copy windows
         return p;
     }
 };
@@ -538,6 +536,8 @@ struct DevCsr {
     float* w32 = nullptr;
     int4 *tiles = nullptr, *longs = nullptr;
     int ntiles = 0, nlong = 0;
+    int nblocks = 0;             // persistent grid of the pipelined kernel
+    bool pipe = true;
     int* counters = nullptr;
     double* tpart = nullptr;
     template <typename T>
@@ -556,7 +556,7 @@ struct DevCsr {
         c.tile_part = tpart;
         return c;
     }
-    int nslots() const { return ntiles + nlong; }
+    int nslots() const { return (pipe ? nblocks : ntiles) + nlong; }
 };
 
 struct hpr_handle {
@@ -598,6 +598,8 @@ struct hpr_handle {
     bool reordered = false;
     int *rperm = nullptr, *cperm = nullptr;
     double* stage = nullptr;     // max(m, n) staging for permuted I/O
+    double* SP = nullptr;        // max(m, n) product vector of the split (unfused) iteration
+    bool fuse = false;           // epilogue fused into the SpMV (HPR_FUSE=1) or separate pass
 };
 
 namespace {
@@ -690,6 +692,7 @@ size_t carve(hpr_handle* h, char* base) {
     h->rperm = cv.take<int>(m);
     h->cperm = cv.take<int>(n);
     h->stage = cv.take<double>(std::max(m, n));
+    h->SP = cv.take<double>(std::max(m, n));
     h->ctrl = cv.take<Ctrl>(1);
     h->d_dev = cv.take<unsigned long long>(2);
     return cv.off + 256;
@@ -842,7 +845,18 @@ double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only) {
 template <typename T, class Epi>
 void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, const Epi& epi,
                  cudaStream_t s) {
-    k_spmv<T, Epi><<<M.ntiles, TPB, 0, s>>>(M.view<T>(vals), xg, epi);
+    if (M.pipe) {
+        static bool attr_set = false;   // one per template instantiation
+        constexpr size_t smem = pipe_smem_bytes<T>();
+        if (!attr_set) {
+            CK(cudaFuncSetAttribute(k_spmv_pipe<T, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+            attr_set = true;
+        }
+        k_spmv_pipe<T, Epi><<<M.nblocks, TPB, smem, s>>>(M.view<T>(vals), xg, epi);
+    } else {
+        k_spmv<T, Epi><<<M.ntiles, TPB, 0, s>>>(M.view<T>(vals), xg, epi);
+    }
     CKL();
     h->launches += 1;
 }
@@ -1017,8 +1031,47 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     h->launches += 2;
 }
 
+// One row-wise pass of an epilogue over a precomputed product vector:
+// the projection / reflection / Halpern update of a whole half-iteration in
+// one coalesced sweep (the split form of the fused SpMV epilogue).
+template <typename T, class Epi>
+__global__ void __launch_bounds__(TPB) k_rowwise(Epi epi, const T* __restrict__ sums, int len) {
+    epi.prepare();
+    Acc<0> acc;
+    for (int j = blockIdx.x * TPB + threadIdx.x; j < len; j += gridDim.x * TPB) {
+        typename Epi::Pre pre;
+        epi.load(j, pre);
+        epi.apply(j, sums[j], pre, acc);
+    }
+}
+
+template <typename T, class Epi>
+void launch_rowwise(hpr_handle* h, const Epi& epi, const T* sums, int len, cudaStream_t s) {
+    k_rowwise<T, Epi><<<std::min(nblk(len), 148 * 16), TPB, 0, s>>>(epi, sums, len);
+    CKL();
+    h->launches += 1;
+}
+
+template <typename T, bool CHECK>
+void enqueue_split(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
+    T* sp = (T*)h->SP;
+    EpiStore<T> st{sp, nullptr};
+    launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, st, s);
+    EpiPrimal<T, CHECK> e1{h->ctrl, j, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
+                           p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
+    launch_rowwise(h, e1, (const T*)sp, h->n, s);
+    launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, st, s);
+    EpiDual<T, CHECK> e2{h->ctrl, j, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
+    launch_rowwise(h, e2, (const T*)sp, h->m, s);
+}
+
 template <typename T>
 void enqueue_iteration(hpr_handle* h, const Ptrs<T>& p, int j, bool check, cudaStream_t s) {
+    if (!h->fuse) {
+        if (check) enqueue_split<T, true>(h, p, j, s);
+        else enqueue_split<T, false>(h, p, j, s);
+        return;
+    }
     if (check) {
         EpiPrimal<T, true> e1{h->ctrl, j, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                               p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
@@ -1367,6 +1420,18 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         h->A.nlong = (int)pa.longs.size();
         h->AT.ntiles = (int)pt.tiles.size();
         h->AT.nlong = (int)pt.longs.size();
+        {
+            int sms = 148;
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
+            const char* fz = getenv("HPR_FUSE");
+            h->fuse = fz && std::string(fz) == "1";
+            const char* mode = getenv("HPR_SPMV");
+            const bool pipe = mode && std::string(mode) == "pipe";
+            for (DevCsr* M : {&h->A, &h->AT}) {
+                M->pipe = pipe;
+                M->nblocks = std::max(1, std::min(M->ntiles, sms * PIPE_CTAS_PER_SM));
+            }
+        }
         CK(cudaMemcpyAsync(h->A.ptr, ptr.data(), sizeof(int) * (p->m + 1), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(h->A.idx, idx.data(), sizeof(int) * p->nnz, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(h->A.mval, val.data(), sizeof(double) * p->nnz, cudaMemcpyHostToDevice, s));
@@ -1639,16 +1704,23 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
     CK(cudaSetDevice(h->dev));
     cudaStream_t s = h->stream;
+    // which: 0 = A x~ product, 1 = A^T y product, 2 = primal row-wise update,
+    //        3 = dual row-wise update, 4 = fused A x~ + dual, 5 = fused A^T y + primal
     auto body = [&](auto tag) {
         using T = decltype(tag);
         Ptrs<T> p = ptrs<T>(h, sizeof(T) == 4);
-        if (which == 0) {
-            EpiDual<T, false> e2{h->ctrl, 0, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
-            launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s);
-        } else {
-            EpiPrimal<T, false> e1{h->ctrl, 0, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                                   p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
-            launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s);
+        T* sp = (T*)h->SP;
+        EpiStore<T> st{sp, nullptr};
+        EpiDual<T, false> e2{h->ctrl, 0, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
+        EpiPrimal<T, false> e1{h->ctrl, 0, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
+                               p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
+        switch (which) {
+            case 0: launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, st, s); break;
+            case 1: launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, st, s); break;
+            case 2: launch_rowwise(h, e1, (const T*)sp, h->n, s); break;
+            case 3: launch_rowwise(h, e2, (const T*)sp, h->m, s); break;
+            case 4: launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s); break;
+            default: launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s); break;
         }
     };
     auto run = [&]() {

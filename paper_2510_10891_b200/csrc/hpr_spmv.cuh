@@ -5,8 +5,8 @@
 // power method lp_kernel.py:157).  The host cuts each CSR operand into
 // tiles of equal work (hpr_engine.cu: build_tiles):
 //
-//  * stream tile  {r0, r1, L, -1}: consecutive rows holding <= TILE_NNZ
-//    nonzeros.  The CTA streams the tile's (value, index) range with fully
+//  * stream tile  {r0, -(r1+1), p0, p1}: consecutive rows holding <= TILE_NNZ
+//    nonzeros and <= TILE_ROWS rows.  The CTA streams the tile's (value, index) range with fully
 //    coalesced evict-first loads, gathers x (L2-resident), and stages the
 //    products in shared memory; then groups of L lanes reduce one row each
 //    (L = 1 for the short structural rows, so those sums run in index order
@@ -65,20 +65,48 @@ __device__ __forceinline__ void block_store(Acc<K>& acc, double* part, int nslot
     }
 }
 
+// Asynchronous global -> shared copy of one 4- or 8-byte element (LDGSTS):
+// the epilogue operands of a tile's rows are staged without occupying
+// registers while the matrix stream and the gathers are in flight.
+template <typename U>
+__device__ __forceinline__ void cp_async_elem(U* dst, const U* src) {
+    static_assert(sizeof(U) == 4 || sizeof(U) == 8, "cp.async element size");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "n"((int)sizeof(U))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// stage vector[r0 + k] (k < R) into column v of the SoA staging buffer
+template <typename U>
+__device__ __forceinline__ void stage_vec(unsigned char* sbuf, int byte_off, const U* vec, int r0,
+                                          int R) {
+    U* dst = reinterpret_cast<U*>(sbuf + byte_off);
+    for (int k = threadIdx.x; k < R; k += TPB) cp_async_elem(dst + k, vec + r0 + k);
+}
+template <typename U>
+__device__ __forceinline__ U unstage_vec(const unsigned char* sbuf, int byte_off, int k) {
+    return reinterpret_cast<const U*>(sbuf + byte_off)[k];
+}
+
 template <typename T, class Epi>
 __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
     __shared__ T prod[TILE_NNZ];
+    __shared__ T rsum[TILE_ROWS];
+    __shared__ int sptr[TILE_ROWS + 1];
     __shared__ T wpart[TPB / 32];
     __shared__ int s_last;
+    __shared__ __align__(16) unsigned char sbuf[Epi::SROW > 0 ? Epi::SROW * TILE_ROWS : 16];
     epi.prepare();
     Acc<Epi::K> acc;
     acc.zero();
     const int4 tl = A.tiles[blockIdx.x];
-    if (tl.w < 0) {
-        // ---------------- stream tile ----------------
-        const int r0 = tl.x, r1 = tl.y, L = tl.z;
-        const int p0 = A.indptr[r0];
-        const int cnt = A.indptr[r1] - p0;
+    if (tl.y < 0) {
+        // ---------------- stream tile {r0, -(r1+1), p0, p1} ----------------
+        const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = tl.w - tl.z;
+        const int R = r1 - r0;
         const int* __restrict__ idx = A.indices + p0;
         const T* __restrict__ val = A.vals + p0;
         int c[ITEMS];
@@ -89,27 +117,45 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg
             c[q] = e < cnt ? ld_stream(idx + e) : 0;
             v[q] = e < cnt ? ld_stream(val + e) : T(0);
         }
+        // row pointers and the epilogue operands of the tile's rows are
+        // fetched while the matrix stream is in flight
+        if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
+        if (threadIdx.x == 0) sptr[R] = cnt;
+        const bool own = threadIdx.x < R;
+        if constexpr (Epi::SROW > 0) {
+            epi.stage(sbuf, r0, R);
+            cp_async_commit();
+        }
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
             const int e = threadIdx.x + q * TPB;
             if (e < cnt) prod[e] = v[q] * ld_ro(xg + c[q]);
         }
         __syncthreads();
+        int L = 1;
+        while (L < 32 && (L * 2) * R <= TPB && L * R < cnt) L *= 2;
         const int lane = threadIdx.x & 31;
         const int gl = threadIdx.x & (L - 1);
         const int grp = threadIdx.x / L;
         const int ngrp = TPB / L;
         const unsigned mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1)));
-        for (int r = r0 + grp; r < r1; r += ngrp) {
-            const int b = A.indptr[r] - p0, e = A.indptr[r + 1] - p0;
+        for (int k = grp; k < R; k += ngrp) {
+            const int b = sptr[k], e = sptr[k + 1];
             T s = T(0);
             for (int q = b + gl; q < e; q += L) s += prod[q];
             for (int off = L >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(mask, s, off);
-            if (gl == 0) epi.row(r, s, acc);
+            if (gl == 0) rsum[k] = s;
+        }
+        if constexpr (Epi::SROW > 0) cp_async_wait_all();
+        __syncthreads();
+        if (own) {
+            typename Epi::Pre pre;
+            epi.unstage(sbuf, threadIdx.x, pre);
+            epi.apply(r0 + threadIdx.x, rsum[threadIdx.x], pre, acc);
         }
         block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
     } else {
-        // ---------------- chunk of a long row ----------------
+        // ---------------- chunk of a long row {row, e0, e1, li} ----------------
         const int row = tl.x, e0 = tl.y, e1 = tl.z, li = tl.w;
         constexpr int IL = CHUNK_NNZ / TPB;
         int c[IL];
@@ -150,7 +196,9 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg
             A.counters[li] = 0;
             Acc<Epi::K> a1;
             a1.zero();
-            epi.row(row, tot, a1);
+            typename Epi::Pre pre;
+            epi.load(row, pre);
+            epi.apply(row, tot, pre, a1);
             if constexpr (Epi::K > 0) {
                 const int nslots = A.ntiles + A.nlong;
 #pragma unroll
@@ -161,26 +209,37 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg
 }
 
 // ---------------------------------------------------------------------------
-// epilogues
+// epilogues: load(r, pre) fetches the row's operands (issued before the
+// product phase), apply(r, sum, pre, acc) finishes the row.
 // ---------------------------------------------------------------------------
 
 // out[r] = (A x)[r]
 template <typename T>
 struct EpiStore {
     static constexpr int K = 0;
+    static constexpr int SROW = 0;
     T* out;
     double* part;
+    struct Pre {};
     __device__ void prepare() {}
-    __device__ __forceinline__ void row(int r, T s, Acc<0>&) { out[r] = s; }
+    __device__ __forceinline__ void load(int, Pre&) const {}
+    __device__ __forceinline__ void stage(unsigned char*, int, int) const {}
+    __device__ __forceinline__ void unstage(const unsigned char*, int, Pre&) const {}
+    __device__ __forceinline__ void apply(int r, T s, const Pre&, Acc<0>&) { out[r] = s; }
 };
 
 // power method step: out = A u, plus sum(out^2) for ||A A^T v|| (lp_kernel.py:157-158)
 struct EpiPower {
     static constexpr int K = 1;
+    static constexpr int SROW = 0;
     double* out;
     double* part;
+    struct Pre {};
     __device__ void prepare() {}
-    __device__ __forceinline__ void row(int r, double s, Acc<1>& a) {
+    __device__ __forceinline__ void load(int, Pre&) const {}
+    __device__ __forceinline__ void stage(unsigned char*, int, int) const {}
+    __device__ __forceinline__ void unstage(const unsigned char*, int, Pre&) const {}
+    __device__ __forceinline__ void apply(int r, double s, const Pre&, Acc<1>& a) {
         out[r] = s;
         a.v[0] += s * s;
     }
@@ -201,6 +260,9 @@ struct EpiPrimal {
     double* part;
     T sig, t, omt;
     double bsc, csc;
+    struct Pre {
+        T x, z, c, lo, up, ax, az;
+    };
     __device__ void prepare() {
         const double sigma = ctrl->sigma;
         const double td = 1.0 / ((double)(ctrl->k0 + j_in_block) + 2.0);
@@ -210,16 +272,45 @@ struct EpiPrimal {
         bsc = ctrl->b_scale;
         csc = ctrl->c_scale;
     }
-    __device__ __forceinline__ void row(int j, T aty, Acc<0>&) {
-        const T x = X[j];
-        const T g = x + sig * (aty - C[j]);
-        const T bx = np_clip(g, LO[j], UP[j]);
+    static constexpr int SROW = 7 * sizeof(T);
+    __device__ __forceinline__ void load(int j, Pre& p) const {
+        p.x = X[j];
+        p.z = Z[j];
+        p.c = C[j];
+        p.lo = LO[j];
+        p.up = UP[j];
+        p.ax = AX[j];
+        p.az = AZ[j];
+    }
+    __device__ __forceinline__ void stage(unsigned char* sb, int r0, int R) const {
+        constexpr int W = TILE_ROWS * sizeof(T);
+        stage_vec(sb, 0 * W, (const T*)X, r0, R);
+        stage_vec(sb, 1 * W, (const T*)Z, r0, R);
+        stage_vec(sb, 2 * W, C, r0, R);
+        stage_vec(sb, 3 * W, LO, r0, R);
+        stage_vec(sb, 4 * W, UP, r0, R);
+        stage_vec(sb, 5 * W, AX, r0, R);
+        stage_vec(sb, 6 * W, AZ, r0, R);
+    }
+    __device__ __forceinline__ void unstage(const unsigned char* sb, int k, Pre& p) const {
+        constexpr int W = TILE_ROWS * sizeof(T);
+        p.x = unstage_vec<T>(sb, 0 * W, k);
+        p.z = unstage_vec<T>(sb, 1 * W, k);
+        p.c = unstage_vec<T>(sb, 2 * W, k);
+        p.lo = unstage_vec<T>(sb, 3 * W, k);
+        p.up = unstage_vec<T>(sb, 4 * W, k);
+        p.ax = unstage_vec<T>(sb, 5 * W, k);
+        p.az = unstage_vec<T>(sb, 6 * W, k);
+    }
+    __device__ __forceinline__ void apply(int j, T aty, const Pre& p, Acc<0>&) {
+        const T g = p.x + sig * (aty - p.c);
+        const T bx = np_clip(g, p.lo, p.up);
         const T bz = (bx - g) / sig;
-        const T xt = T(2) * bx - x;
-        const T zh = T(2) * bz - Z[j];
+        const T xt = T(2) * bx - p.x;
+        const T zh = T(2) * bz - p.z;
         XT[j] = xt;
-        X[j] = t * AX[j] + omt * xt;
-        Z[j] = t * AZ[j] + omt * zh;
+        X[j] = t * p.ax + omt * xt;
+        Z[j] = t * p.az + omt * zh;
         if constexpr (CHECK) {
             BX[j] = bx;
             BZ[j] = bz;
@@ -245,6 +336,9 @@ struct EpiDual {
     double* part;
     T inv, t, omt;
     double csc;
+    struct Pre {
+        T y, rhs, ay;
+    };
     __device__ void prepare() {
         const double td = 1.0 / ((double)(ctrl->k0 + j_in_block) + 2.0);
         inv = (T)(1.0 / (ctrl->lam * ctrl->sigma));
@@ -252,12 +346,29 @@ struct EpiDual {
         omt = (T)(1.0 - td);
         csc = ctrl->c_scale;
     }
-    __device__ __forceinline__ void row(int i, T ax, Acc<0>&) {
-        const T y = Y[i];
-        const T v = y + inv * (RHS[i] - ax);
+    static constexpr int SROW = 3 * sizeof(T);
+    __device__ __forceinline__ void load(int i, Pre& p) const {
+        p.y = Y[i];
+        p.rhs = RHS[i];
+        p.ay = AY[i];
+    }
+    __device__ __forceinline__ void stage(unsigned char* sb, int r0, int R) const {
+        constexpr int W = TILE_ROWS * sizeof(T);
+        stage_vec(sb, 0 * W, (const T*)Y, r0, R);
+        stage_vec(sb, 1 * W, RHS, r0, R);
+        stage_vec(sb, 2 * W, AY, r0, R);
+    }
+    __device__ __forceinline__ void unstage(const unsigned char* sb, int k, Pre& p) const {
+        constexpr int W = TILE_ROWS * sizeof(T);
+        p.y = unstage_vec<T>(sb, 0 * W, k);
+        p.rhs = unstage_vec<T>(sb, 1 * W, k);
+        p.ay = unstage_vec<T>(sb, 2 * W, k);
+    }
+    __device__ __forceinline__ void apply(int i, T ax, const Pre& p, Acc<0>&) {
+        const T v = p.y + inv * (p.rhs - ax);
         const T by = i >= n_eq ? np_max(v, T(0)) : v;
-        const T yh = T(2) * by - y;
-        Y[i] = t * AY[i] + omt * yh;
+        const T yh = T(2) * by - p.y;
+        Y[i] = t * p.ay + omt * yh;
         if constexpr (CHECK) {
             BY[i] = by;
             YM[i] = ((double)by * RS[i]) * csc;
@@ -274,18 +385,41 @@ struct EpiCheckRows {
     const double *YM, *RHSM;
     const T *BY, *AY;
     double* part;
+    struct Pre {
+        double ym, rhs;
+        T by, ay;
+    };
     __device__ void prepare() {}
-    __device__ __forceinline__ void row(int i, double ax, Acc<KR>& a) {
-        const double ym = YM[i];
-        const double v = (ym - ax) + RHSM[i];
+    static constexpr int SROW = 2 * 8 + 2 * sizeof(T);
+    __device__ __forceinline__ void load(int i, Pre& p) const {
+        p.ym = YM[i];
+        p.rhs = RHSM[i];
+        p.by = BY[i];
+        p.ay = AY[i];
+    }
+    __device__ __forceinline__ void stage(unsigned char* sb, int r0, int R) const {
+        constexpr int D = TILE_ROWS * 8, W = TILE_ROWS * sizeof(T);
+        stage_vec(sb, 0, YM, r0, R);
+        stage_vec(sb, D, RHSM, r0, R);
+        stage_vec(sb, 2 * D, BY, r0, R);
+        stage_vec(sb, 2 * D + W, AY, r0, R);
+    }
+    __device__ __forceinline__ void unstage(const unsigned char* sb, int k, Pre& p) const {
+        constexpr int D = TILE_ROWS * 8, W = TILE_ROWS * sizeof(T);
+        p.ym = unstage_vec<double>(sb, 0, k);
+        p.rhs = unstage_vec<double>(sb, D, k);
+        p.by = unstage_vec<T>(sb, 2 * D, k);
+        p.ay = unstage_vec<T>(sb, 2 * D + W, k);
+    }
+    __device__ __forceinline__ void apply(int i, double ax, const Pre& p, Acc<KR>& a) {
+        const double v = (p.ym - ax) + p.rhs;
         const double pr = i >= n_eq ? np_max(v, 0.0) : v;
-        const double pv = ym - pr;
+        const double pv = p.ym - pr;
         a.v[0] += pv * pv;
-        a.v[1] += RHSM[i] * ym;
-        const T by = BY[i];
-        const double d = (double)(by - AY[i]);
+        a.v[1] += p.rhs * p.ym;
+        const double d = (double)(p.by - p.ay);
         a.v[2] += d * d;
-        a.v[3] += finite(by) ? 0.0 : 1.0;
+        a.v[3] += finite(p.by) ? 0.0 : 1.0;
     }
 };
 
@@ -297,21 +431,55 @@ struct EpiCheckCols {
     const double *XM, *ZM, *COSTM, *LOM, *UPM;
     const T *BX, *BZ, *AX;
     double* part;
+    struct Pre {
+        double xm, zm, c, lo, up;
+        T bx, bz, ax;
+    };
     __device__ void prepare() {}
-    __device__ __forceinline__ void row(int j, double aty, Acc<KC>& a) {
-        const double xm = XM[j], zm = ZM[j];
-        const double lo = LOM[j], up = UPM[j];
-        const double dv = (COSTM[j] - aty) - zm;
-        const double bv = xm - np_clip(xm - zm, lo, up);
+    static constexpr int SROW = 5 * 8 + 3 * sizeof(T);
+    __device__ __forceinline__ void load(int j, Pre& p) const {
+        p.xm = XM[j];
+        p.zm = ZM[j];
+        p.c = COSTM[j];
+        p.lo = LOM[j];
+        p.up = UPM[j];
+        p.bx = BX[j];
+        p.bz = BZ[j];
+        p.ax = AX[j];
+    }
+    __device__ __forceinline__ void stage(unsigned char* sb, int r0, int R) const {
+        constexpr int D = TILE_ROWS * 8, W = TILE_ROWS * sizeof(T);
+        stage_vec(sb, 0 * D, XM, r0, R);
+        stage_vec(sb, 1 * D, ZM, r0, R);
+        stage_vec(sb, 2 * D, COSTM, r0, R);
+        stage_vec(sb, 3 * D, LOM, r0, R);
+        stage_vec(sb, 4 * D, UPM, r0, R);
+        stage_vec(sb, 5 * D, BX, r0, R);
+        stage_vec(sb, 5 * D + W, BZ, r0, R);
+        stage_vec(sb, 5 * D + 2 * W, AX, r0, R);
+    }
+    __device__ __forceinline__ void unstage(const unsigned char* sb, int k, Pre& p) const {
+        constexpr int D = TILE_ROWS * 8, W = TILE_ROWS * sizeof(T);
+        p.xm = unstage_vec<double>(sb, 0 * D, k);
+        p.zm = unstage_vec<double>(sb, 1 * D, k);
+        p.c = unstage_vec<double>(sb, 2 * D, k);
+        p.lo = unstage_vec<double>(sb, 3 * D, k);
+        p.up = unstage_vec<double>(sb, 4 * D, k);
+        p.bx = unstage_vec<T>(sb, 5 * D, k);
+        p.bz = unstage_vec<T>(sb, 5 * D + W, k);
+        p.ax = unstage_vec<T>(sb, 5 * D + 2 * W, k);
+    }
+    __device__ __forceinline__ void apply(int j, double aty, const Pre& p, Acc<KC>& a) {
+        const double dv = (p.c - aty) - p.zm;
+        const double bv = p.xm - np_clip(p.xm - p.zm, p.lo, p.up);
         a.v[0] += dv * dv;
         a.v[1] += bv * bv;
-        a.v[2] += COSTM[j] * xm;
-        a.v[3] += isfinite(lo) ? lo * np_max(zm, 0.0) : 0.0;
-        a.v[4] += isfinite(up) ? up * np_min(zm, 0.0) : 0.0;
-        const T bx = BX[j];
-        const double d = (double)(bx - AX[j]);
+        a.v[2] += p.c * p.xm;
+        a.v[3] += isfinite(p.lo) ? p.lo * np_max(p.zm, 0.0) : 0.0;
+        a.v[4] += isfinite(p.up) ? p.up * np_min(p.zm, 0.0) : 0.0;
+        const double d = (double)(p.bx - p.ax);
         a.v[5] += d * d;
-        a.v[6] += (finite(bx) ? 0.0 : 1.0) + (finite(BZ[j]) ? 0.0 : 1.0);
+        a.v[6] += (finite(p.bx) ? 0.0 : 1.0) + (finite(p.bz) ? 0.0 : 1.0);
     }
 };
 
