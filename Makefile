@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 FLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -Xcompiler -fPIC -shared
 SRC := paper_2510_10891_b200/csrc/hpr_engine.cu
-DEPS := $(SRC) paper_2510_10891_b200/csrc/hpr_common.cuh paper_2510_10891_b200/csrc/hpr_spmv.cuh include/hprlp_b200.h
+DEPS := $(SRC) $(wildcard paper_2510_10891_b200/csrc/*.cuh) include/hprlp_b200.h
 LIB := paper_2510_10891_b200/libhprlp_b200.so
 
 all: $(LIB)

@@ -191,6 +191,7 @@ def run_b200(args):
     s = 8 if args.precision == "fp64" else 4
     lp = lpa.to_lp()
     eng = hprlp.Engine(lp, device=local)
+    lay = eng.layout()
     cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(args.precision),
                              max_iterations=max(1, args.warmup) * BLOCK)
     x, y, z, st0, _ = eng.solve_raw(cfg)                  # setup + W warm-up blocks
@@ -214,6 +215,11 @@ def run_b200(args):
     value = ws * its / t_loop
 
     bm = bytes_model(m, n, nnz, s)
+    nf, nnzf = lay["folded_rows"], lay["folded_nnz"]
+    stored = {"spmv_A": nnzf * (s + 4) + 4 * (nf + 1) + s * n + s * nf,
+              "spmv_AT": nnzf * (s + 4) + 4 * (n + 1) + s * nf + s * n,
+              "update_primal": bm["update_primal"],
+              "update_dual": s * (4 * m + 2 * nf)}
     peak, peak_kind = measured_peak_hbm()
     dom = max(ktimes, key=ktimes.get)
     dom_t, dom_b = ktimes[dom], bm[dom]
@@ -229,11 +235,19 @@ def run_b200(args):
         "config": {"workload": f"{args.config}: synthetic 13659-bus/4092-unit/36-period SCUC "
                                f"LP relaxation + {args.triples or 1000} base flow triples",
                    "rows": m, "cols": n, "nnz": nnz, "step": "16 HPR iterations + KKT check",
+                   "device_layout": {"folded_rows": lay["folded_rows"],
+                                     "folded_nnz": lay["folded_nnz"],
+                                     "reordered": bool(lay["reordered"]),
+                                     "twin_folded": bool(lay["folded"])},
                    "l2": "inputs larger than L2 (matrix stream > 1 GB/iteration)",
                    "parallelism": f"replicas{ws}" if ws > 1 else "single"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                      "bytes_per_launch": dom_b, "seconds_per_launch": dom_t,
+                     "bytes_basis": "CSR-equivalent algorithmic bytes (SURVEY 8(d)); the "
+                                    "engine stores twin rows once, so its DRAM traffic "
+                                    "(ncu 'traffic') is lower",
+                     "stored_bytes_per_launch": stored[dom],
                      "peak_kind": peak_kind},
         "iteration_roofline": {"bytes_per_iteration": bm["iter"], "achieved_gbs": it_gbs,
                                "frac": it_gbs / peak},

@@ -19,11 +19,13 @@ LIB_PATH = os.path.join(HERE, LIB_NAME)
 HPR_OPTIMAL, HPR_ITERATION_LIMIT, HPR_TIME_LIMIT, HPR_NUMERICAL_FAILURE = 0, 1, 2, 3
 HPR_FP64, HPR_FP32 = 0, 1
 HPR_FLAG_NO_REORDER = 1
+HPR_FLAG_NO_FOLD = 2
 HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
            "hpr_destroy", "hpr_solve", "hpr_get_log", "hpr_matvec", "hpr_kkt_residual",
-           "hpr_power_method", "hpr_iterate", "hpr_resume", "hpr_bench_kernel")
+           "hpr_power_method", "hpr_iterate", "hpr_resume", "hpr_bench_kernel",
+           "hpr_get_layout")
 
 _p = C.c_void_p
 
@@ -76,6 +78,14 @@ class LogRecord(C.Structure):
                                   "primal", "box", "dual")]
 
 
+class Layout(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32), ("n_eq", C.c_int32),
+                ("folded_rows", C.c_int32), ("nnz", C.c_int64), ("folded_nnz", C.c_int64),
+                ("tiles_a", C.c_int32), ("tiles_at", C.c_int32), ("tiles_f", C.c_int32),
+                ("tiles_ft", C.c_int32), ("reordered", C.c_int32), ("folded", C.c_int32),
+                ("workspace_bytes", C.c_size_t)]
+
+
 class HprError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libhprlp_b200 error {code}: {msg}")
@@ -111,6 +121,7 @@ def load(path: str | None = None):
     lib.hpr_iterate.argtypes = [_p, C.c_int32, C.c_double, C.c_double, C.c_int64] + [_p] * 12
     lib.hpr_resume.argtypes = [_p, C.c_int64, C.c_double, C.POINTER(Stats)]
     lib.hpr_bench_kernel.argtypes = [_p, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+    lib.hpr_get_layout.argtypes = [_p, C.POINTER(Layout)]
     _LIB = lib
     return lib
 

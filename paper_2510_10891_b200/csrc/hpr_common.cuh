@@ -82,7 +82,7 @@ struct Csr {
     const int4* longs;       // {row, first_tile, nchunks, 0}
     int nlong;
     int* counters;           // per long row, zero between launches
-    double* tile_part;       // per tile partial sums of long-row chunks
+    double* tile_part;       // per tile partial sums of long-row chunks (work dtype)
 };
 
 }  // namespace hpr

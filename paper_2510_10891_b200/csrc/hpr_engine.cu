@@ -1,23 +1,24 @@
-// hpr_engine.cu — B200 HPR-LP engine: setup kernels, on-device controller,
-// CUDA-graph iteration loop, and the C-ABI declared in include/hprlp_b200.h.
+// hpr_engine.cu — B200 HPR-LP engine: host orchestration, CUDA-graph
+// iteration loop and the C-ABI declared in include/hprlp_b200.h.
 //
 // Reference path replaced: scuckit.hprlp._solve_once (hprlp.py:332-455) with
 // its scaling (_ScaleMaps :210-276), power method (lp_kernel.py:138-175),
 // iteration (hpr_iterate :184-207) and KKT checks (kkt_residual :116-139).
 //
 // Data layout in HBM (one workspace, 256-byte aligned sub-arrays):
-//   A   : CSR  indptr[m+1] i32, indices[nnz] i32, master values f64,
-//         work values f64 (scaled) and f32 (FP32 mode)
-//   A^T : the same for the transpose (built once, host counting sort)
-//   tile schedules of A and A^T (int4), long-row tickets and chunk partials
+//   A, A^T  : CSR int32 indptr/indices, FP64 master values, FP64 scaled
+//             values — used for scaling, the power method and matvec
+//   F, F^T  : the twin-folded operands the iteration and the check use
+//             (hpr_update.cuh): int32 indptr/indices, FP64 master values,
+//             FP64 + FP32 work values, gather map into the unfolded values
+//   tile schedules (int4) for the four operands, long-row tickets, partials
 //   master vectors (rhs, cost, lower, upper) f64, scalings rs[m], cs[n]
-//   work vectors in the work dtype: x, z, x~ (=2 bar_x - x), anchors, bars
-//   master bar triple (x, y, z) f64 and the best master triple
-//   check partial sums (slot-major, one slot per tile / long row), Ctrl, log
+//   work vectors in the work dtype: x, z, x~, anchors, bars, y_fold, products
+//   master bar triple and best triple (f64), check partial sums, Ctrl, log
 //
-// Per HPR block of B = check_every iterations the graph body launches
-//   B x { spmv<EpiPrimal>(A^T, y), spmv<EpiDual>(A, x~) }      fused iteration
-//   spmv<EpiCheckRows>(A_master, x_m), spmv<EpiCheckCols>(A^T_master, y_m)
+// Per block of B = check_every iterations the graph body launches
+//   B x { spmv(F^T, y_fold) -> p; update_primal(p); spmv(F, x~) -> p; update_dual(p) }
+//   spmv(F_m, x_m), check_rows, spmv(F^T_m, y_m_fold), check_cols
 //   k_controller (convergence / best / restart / sigma; sets the WHILE flag)
 //   k_restart_copy (best save + anchor reset, no-op unless flagged)
 // inside a conditional WHILE graph node: the host launches one graph per
@@ -28,13 +29,15 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "hpr_common.cuh"
+#include "hpr_setup.cuh"
 #include "hpr_spmv.cuh"
-#include "hpr_spmv_pipe.cuh"
+#include "hpr_update.cuh"
 #include "../../include/hprlp_b200.h"
 
 using namespace hpr;
@@ -63,422 +66,19 @@ static void fail(int code, const std::string& msg) {
 
 #define CKL() CK(cudaGetLastError())
 
-// ===========================================================================
-// setup kernels (scaling: hprlp.py:213-264, lp_kernel.py:105-122)
-// ===========================================================================
-
-__global__ void k_fill(double* p, double v, long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        p[i] = v;
-}
-
-// ||row||_inf of |A| (max is order-independent): one warp per row
-__global__ void k_row_absmax(const int* ptr, const double* vals, int rows, double* out) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= rows) return;
-    double m = 0.0;
-    for (int e = ptr[warp] + lane; e < ptr[warp + 1]; e += 32) m = fmax(m, fabs(vals[e]));
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) out[warp] = m;
-}
-
-// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src),
-// which scipy's abs(A).sum(axis) reaches through np.add.reduceat:
-// segment sum = a[0] + pairwise(a[1:]).  Leaves of <= 128 elements use 8
-// strided accumulators; larger ranges split at a multiple of 8 below n/2.
-// The recursion is unrolled onto a small explicit stack (the default device
-// stack is too small for deep recursion on ~20K-entry rows).
-__device__ double np_pairwise_leaf(const double* a, int n) {
-    if (n < 8) {
-        double r = 0.0;
-        for (int i = 0; i < n; ++i) r += fabs(a[i]);
-        return r;
-    }
-    double r[8];
-    for (int k = 0; k < 8; ++k) r[k] = fabs(a[k]);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-        for (int k = 0; k < 8; ++k) r[k] += fabs(a[i + k]);
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += fabs(a[i]);
-    return res;
-}
-
-__device__ double np_pairwise_abs(const double* a, int n) {
-    int off[32], len[32], state[32];
-    double left[32];
-    int sp = 0;
-    off[0] = 0;
-    len[0] = n;
-    state[0] = 0;
-    double ret = 0.0;
-    while (sp >= 0) {
-        if (len[sp] <= 128) {
-            ret = np_pairwise_leaf(a + off[sp], len[sp]);
-            --sp;
-            continue;
-        }
-        int n2 = len[sp] / 2;
-        n2 -= n2 % 8;
-        if (state[sp] == 0) {
-            state[sp] = 1;
-            off[sp + 1] = off[sp];
-            len[sp + 1] = n2;
-            state[sp + 1] = 0;
-            ++sp;
-        } else if (state[sp] == 1) {
-            left[sp] = ret;
-            state[sp] = 2;
-            off[sp + 1] = off[sp] + n2;
-            len[sp + 1] = len[sp] - n2;
-            state[sp + 1] = 0;
-            ++sp;
-        } else {
-            ret = left[sp] + ret;
-            --sp;
-        }
-    }
-    return ret;
-}
-
-__global__ void k_row_abssum(const int* ptr, const double* vals, int rows, double* out) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const int b = ptr[r], n = ptr[r + 1] - b;
-    out[r] = n == 0 ? 0.0 : fabs(vals[b]) + np_pairwise_abs(vals + b + 1, n - 1);
-}
-
-__device__ __forceinline__ void atomic_max_pos(unsigned long long* p, double v) {
-    // v >= 0: IEEE ordering equals unsigned ordering of the bit pattern
-    atomicMax(p, (unsigned long long)__double_as_longlong(v));
-}
-
-// f = 1/sqrt(where(norm > 0, norm, 1)); scale *= f; dev = max |1 - f|   (hprlp.py:222-231)
-__global__ void k_scale_factor(const double* norm, double* f, double* scale, int n,
-                               unsigned long long* dev) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double d = 0.0;
-    if (i < n) {
-        const double v = norm[i];
-        const double r = 1.0 / sqrt(v > 0 ? v : 1.0);
-        f[i] = r;
-        scale[i] = scale[i] * r;
-        d = fabs(1.0 - r);
-    }
-    for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
-    if ((threadIdx.x & 31) == 0 && dev) atomic_max_pos(dev, d);
-}
-
-// D_r A D_c with the reference rounding (a * r_i) * c_j  (lp_kernel.py:118-122).
-// For the transpose copy row factor and column factor swap roles, the
-// product order stays (a * r_i) * c_j.  One warp per row.
-__global__ void k_scale_csr(const int* ptr, const int* idx, double* vals, int rows,
-                            const double* rowf, const double* colf, int transposed) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= rows) return;
-    const double rf = rowf[warp];
-    for (int e = ptr[warp] + lane; e < ptr[warp + 1]; e += 32) {
-        const double cf = colf[idx[e]];
-        vals[e] = transposed ? (vals[e] * cf) * rf : (vals[e] * rf) * cf;
-    }
-}
-
-// rhs*R, cost*C, bounds/C where finite   (hprlp.py:243-246)
-__global__ void k_work_cols(int n, const double* cost, const double* lo, const double* up,
-                            const double* cs, double* cw, double* low, double* upw) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const double c = cs[j];
-    cw[j] = cost[j] * c;
-    low[j] = isfinite(lo[j]) ? lo[j] / c : lo[j];
-    upw[j] = isfinite(up[j]) ? up[j] / c : up[j];
-}
-
-__global__ void k_work_rows(int m, const double* rhs, const double* rs, double* rw) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) rw[i] = rhs[i] * rs[i];
-}
-
-// rhs/b, cost/c, bounds/b where finite   (hprlp.py:256-259)
-__global__ void k_norm_cols(int n, double bsc, double csc, double* cw, double* low, double* upw) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    cw[j] = cw[j] / csc;
-    if (isfinite(low[j])) low[j] = low[j] / bsc;
-    if (isfinite(upw[j])) upw[j] = upw[j] / bsc;
-}
-
-__global__ void k_div(double* v, long long n, double s) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        v[i] = v[i] / s;
-}
-
-// deterministic two-pass sum of squares (optionally of finite entries only)
-constexpr int RED_BLOCKS = 296;
-__global__ void k_sumsq_part(const double* v, long long n, int finite_only, double* part) {
-    double s = 0.0;
-    for (long long i = blockIdx.x * (long long)TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
-        const double x = v[i];
-        if (!finite_only || isfinite(x)) s += x * x;
-    }
-    __shared__ double w[TPB / 32];
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int k = 0; k < TPB / 32; ++k) t += w[k];
-        part[blockIdx.x] = t;
-    }
-}
-
-__global__ void k_sum_slots(const double* part, int nslots, int nq, double* out) {
-    // one CTA; out[q] = sum_s part[q*nslots + s] in a fixed order
-    __shared__ double w[TPB / 32];
-    for (int q = 0; q < nq; ++q) {
-        double s = 0.0;
-        for (int i = threadIdx.x; i < nslots; i += TPB) s += part[(size_t)q * nslots + i];
-        s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int k = 0; k < TPB / 32; ++k) t += w[k];
-            out[q] = t;
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void k_cast_f32(const double* in, float* out, long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
-        out[i] = (float)in[i];
-}
-
-// initial point (hprlp.py:357-365): to_work, box projection with the FP64
-// work bounds, cast to the work dtype; anchors and bars start equal; master
-// copies for the initial residual (to_master, :272-276).
-template <typename T>
-__global__ void k_init_cols(int n, const double* x0, const double* z0, const double* cs,
-                            double bsc, double csc, const double* low, const double* upw,
-                            T* X, T* Z, T* AX, T* AZ, T* BX, T* BZ, double* XM, double* ZM) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const double c = cs[j];
-    double xw = 0.0, zw = 0.0;
-    if (x0) {
-        xw = x0[j] / (c * bsc);
-        zw = z0[j] * c / csc;
-    }
-    xw = np_clip(xw, low[j], upw[j]);
-    const T x = (T)xw, z = (T)zw;
-    X[j] = AX[j] = BX[j] = x;
-    Z[j] = AZ[j] = BZ[j] = z;
-    XM[j] = ((double)x * c) * bsc;
-    ZM[j] = ((double)z * csc) / c;
-}
-
-template <typename T>
-__global__ void k_init_rows(int m, const double* y0, const double* rs, double csc, T* Y, T* AY,
-                            T* BY, double* YM) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const double r = rs[i];
-    const double yw = y0 ? y0[i] / (r * csc) : 0.0;
-    const T y = (T)yw;
-    Y[i] = AY[i] = BY[i] = y;
-    YM[i] = ((double)y * r) * csc;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-__global__ void k_set_deadline(Ctrl* c, unsigned long long remaining_ns) {
-    c->deadline_ns = globaltimer() + remaining_ns;
-}
-
-// ===========================================================================
-// controller (hprlp.py:403-446) — one CTA, no host round trip
-// ===========================================================================
-
-constexpr int CTRL_TPB = 512;
-
-__global__ void __launch_bounds__(CTRL_TPB)
-k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int nc, LogRec* log,
-             int mode) {
-    __shared__ double sums[KR + KC];
-    __shared__ double w[CTRL_TPB / 32];
-    for (int q = 0; q < KR + KC; ++q) {
-        const double* p = q < KR ? rowpart + (size_t)q * nr : colpart + (size_t)(q - KR) * nc;
-        const int ns = q < KR ? nr : nc;
-        double s = 0.0;
-        for (int i = threadIdx.x; i < ns; i += CTRL_TPB) s += p[i];
-        s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int k = 0; k < CTRL_TPB / 32; ++k) t += w[k];
-            sums[q] = t;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x != 0) return;
-
-    const double s_p = sums[0], s_ry = sums[1], s_dy = sums[2], nf_y = sums[3];
-    const double s_d = sums[KR + 0], s_b = sums[KR + 1], s_cx = sums[KR + 2];
-    const double s_lo = sums[KR + 3], s_up = sums[KR + 4], s_dx = sums[KR + 5], nf_x = sums[KR + 6];
-
-    if (mode == 1) {
-        const long long tnow = c->total + c->B;
-        c->total = tnow;
-        c->flag_improved = 0;
-        c->flag_restart = 0;
-        if (nf_y + nf_x > 0.0) {               // hprlp.py:406-409
-            c->status = HPR_NUMERICAL_FAILURE;
-            if (c->cond) cudaGraphSetConditional(c->cond, 0);
-            return;
-        }
-    }
-
-    // KktResidual fields (hprlp.py:127-139)
-    double r[10];
-    r[0] = sqrt(s_p);
-    r[1] = sqrt(s_b);
-    r[2] = sqrt(s_d);
-    r[3] = r[0] / c->denom;
-    r[4] = r[1] / c->denom;
-    r[5] = r[2] / c->denom;
-    r[6] = s_cx + c->offset;
-    r[7] = (s_ry + (s_lo + s_up)) + c->offset;
-    r[8] = fabs(r[6] - r[7]);
-    r[9] = r[8] / ((1.0 + fabs(r[6])) + fabs(r[7]));
-    double mr = r[3];                          // builtin max(rel_p, rel_b, rel_d, rel_gap)
-    if (r[4] > mr) mr = r[4];
-    if (r[5] > mr) mr = r[5];
-    if (r[9] > mr) mr = r[9];
-    for (int k = 0; k < 10; ++k) c->cur[k] = r[k];
-
-    auto best_max = [&]() {
-        double b = c->best[3];
-        if (c->best[4] > b) b = c->best[4];
-        if (c->best[5] > b) b = c->best[5];
-        if (c->best[9] > b) b = c->best[9];
-        return b;
-    };
-
-    if (mode == 0) {                           // initial residual (hprlp.py:371-391)
-        for (int k = 0; k < 10; ++k) c->best[k] = r[k];
-        c->last_restart_res = mr;
-        c->epoch_min = mr;
-        c->last_improvement = 0;
-        c->flag_improved = 1;
-        c->flag_restart = 0;
-        c->status = (mr <= c->tol) ? HPR_OPTIMAL : -1;
-        return;
-    }
-
-    const long long tnow = c->total;
-    c->checks += 1;
-    if (c->log_on && c->n_log < c->log_cap) {  // hprlp.py:412-420
-        LogRec& L = log[c->n_log++];
-        L.iteration = tnow;
-        L.epoch = c->epoch;
-        L.k = c->k0 + c->B;
-        L.rel_primal = r[3];
-        L.rel_dual = r[5];
-        L.rel_box = r[4];
-        L.rel_gap = r[9];
-        L.sigma = c->sigma;
-        L.primal = r[0];
-        L.box = r[1];
-        L.dual = r[2];
-    }
-    int improved = 0;
-    if (mr < best_max()) improved = 1;                         // :422-424
-    if (mr < c->epoch_min * (1.0 - 1e-12)) {                  // :425-427
-        c->epoch_min = mr;
-        c->last_improvement = tnow;
-    }
-    int restart = 0;
-    if (mr <= c->tol) {                                        // :429-432
-        improved = 1;
-        c->status = HPR_OPTIMAL;
-    } else {
-        const bool suff = mr <= c->beta * c->last_restart_res;  // :434-436
-        const bool stalled = tnow - c->last_improvement >= c->stall;
-        if (suff || stalled) {
-            const double dx = sqrt(s_dx), dy = sqrt(s_dy);       // :437-441
-            if (dx > 1e-14 && dy > 1e-14 && c->norm_a > 0) {
-                const double ratio = dx / (c->norm_a * dy * c->sigma);
-                double f = c->damping == 0.5 ? sqrt(ratio) : pow(ratio, c->damping);
-                f = np_min(np_max(f, 0.25), 4.0);
-                c->sigma = c->sigma * f;
-            }
-            restart = 1;                                       // :442-446
-            c->k0 = 0;
-            c->epoch += 1;
-            c->restarts += 1;
-            c->last_restart_res = mr;
-            c->epoch_min = mr;
-            c->last_improvement = tnow;
-        } else {
-            c->k0 += c->B;
-        }
-    }
-    if (improved)
-        for (int k = 0; k < 10; ++k) c->best[k] = r[k];
-    c->flag_improved = improved;
-    c->flag_restart = restart;
-    if (c->status == -1) {                                     // :394-399
-        if (tnow + c->B > c->max_iter) c->status = HPR_ITERATION_LIMIT;
-        else if (c->has_deadline && globaltimer() > c->deadline_ns) c->status = HPR_TIME_LIMIT;
-    }
-    if (c->cond) cudaGraphSetConditional(c->cond, c->status == -1 ? 1u : 0u);
-}
-
-// best-triple save and restart copies (hprlp.py:172-181, 422-424, 430)
-template <typename T>
-__global__ void k_restart_copy(const Ctrl* c, int n, int m, const double* XM, const double* YM,
-                               const double* ZM, double* BXm, double* BYm, double* BZm, T* X,
-                               T* Y, T* Z, T* AX, T* AY, T* AZ, const T* BX, const T* BY,
-                               const T* BZ) {
-    const int imp = c->flag_improved, rst = c->flag_restart;
-    if (!imp && !rst) return;
-    const int len = n > m ? n : m;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
-        if (i < n) {
-            if (imp) {
-                BXm[i] = XM[i];
-                BZm[i] = ZM[i];
-            }
-            if (rst) {
-                const T bx = BX[i], bz = BZ[i];
-                X[i] = AX[i] = bx;
-                Z[i] = AZ[i] = bz;
-            }
-        }
-        if (i < m) {
-            if (imp) BYm[i] = YM[i];
-            if (rst) {
-                const T by = BY[i];
-                Y[i] = AY[i] = by;
-            }
-        }
-    }
-}
-
-// ===========================================================================
-// host side
-// ===========================================================================
-
 namespace {
+
+inline int nblk(long long n, int tpb = TPB) {
+    return (int)std::max<long long>(1, (n + tpb - 1) / tpb);
+}
+
+// fixed grid of the row-wise passes: deterministic partial-sum slots
+constexpr int ROW_GRID_MAX = 148 * 8;
+inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
+
+// ===========================================================================
+// tile schedule
+// ===========================================================================
 
 struct Plan {
     std::vector<int4> tiles, longs;
@@ -515,6 +115,20 @@ Plan build_tiles(const int32_t* ptr, int rows) {
     return p;
 }
 
+// Upper bounds on the schedule of a CSR, independent of row order and folding
+// (so the workspace can be sized from (m, n, nnz) alone).  A stream tile
+// closes on a full row count, on nnz overflow (two consecutive tiles then hold
+// more than TILE_NNZ), before a long row, or at the end.
+struct TileBound {
+    size_t tiles, longs;
+};
+TileBound tile_bound(long long rows, long long nnz) {
+    const long long nlong = std::min<long long>(rows, nnz / (TILE_NNZ + 1));
+    const long long t = 2 * (nnz / TILE_NNZ + 1) + rows / TILE_ROWS + 1 + 2 * nlong +
+                        (nnz / CHUNK_NNZ + 1) + nlong + 2;
+    return {(size_t)t, (size_t)std::max<long long>(nlong, 1)};
+}
+
 struct Carver {
     size_t off = 0;
     char* base = nullptr;
@@ -522,22 +136,23 @@ struct Carver {
     T* take(size_t count) {
         off = (off + 255) & ~size_t(255);
         T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
-        off += sizeof(T) * std::max<size_t>(count, 1) + 64;   // tail pad: 16-byte bulk-copy windows
+        off += sizeof(T) * std::max<size_t>(count, 1) + 64;
         return p;
     }
 };
 
 }  // namespace
 
+// A CSR operand on the device with its schedule.
 struct DevCsr {
     int rows = 0, cols = 0;
+    long long nnz = 0;
     int *ptr = nullptr, *idx = nullptr;
     double *mval = nullptr, *w64 = nullptr;
     float* w32 = nullptr;
+    int* src = nullptr;          // folded operands: source entry in the unfolded values
     int4 *tiles = nullptr, *longs = nullptr;
     int ntiles = 0, nlong = 0;
-    int nblocks = 0;             // persistent grid of the pipelined kernel
-    bool pipe = true;
     int* counters = nullptr;
     double* tpart = nullptr;
     template <typename T>
@@ -556,28 +171,30 @@ struct DevCsr {
         c.tile_part = tpart;
         return c;
     }
-    int nslots() const { return (pipe ? nblocks : ntiles) + nlong; }
+    int nslots() const { return ntiles + nlong; }
 };
 
 struct hpr_handle {
     int dev = 0;
     cudaStream_t stream = nullptr, cap = nullptr;
     bool own_stream = false;
-    int m = 0, n = 0, n_eq = 0;
-    long long nnz = 0;
+    int m = 0, n = 0, n_eq = 0, nf = 0;
+    long long nnz = 0, nnz_f = 0;
     double offset = 0.0;
-    DevCsr A, AT;
-    // vectors
+    DevCsr A, AT, F, FT;
+    bool folded = false;
+    int* frow = nullptr;                     // nf + 1 folded-row starts
+    // vectors (engine order)
     double *rhs_m, *cost_m, *lo_m, *up_m, *rs, *cs, *fr, *fc;
-    double *rhs_w, *cost_w, *lo_w, *up_w;   // FP64 work (setup)
-    void *rhsT, *costT, *loT, *upT;          // work dtype copies (FP32 mode)
-    void *X, *Y, *Z, *AXv, *AYv, *AZv, *XT, *BX, *BY, *BZ;
-    double *XM, *YM, *ZM, *BXm, *BYm, *BZm;
-    double *rowpart, *colpart, *red, *pw;   // pw: power-method vectors (m + n)
+    double *rhs_w, *cost_w, *lo_w, *up_w;    // FP64 work (setup)
+    void *rhsT, *costT, *loT, *upT;           // work dtype copies (FP32 mode)
+    void *X, *Y, *Z, *AXv, *AYv, *AZv, *XT, *BX, *BY, *BZ, *YF, *BYF, *P;
+    double *XM, *YM, *ZM, *YMF, *BXm, *BYm, *BZm;
+    double *rowpart, *colpart, *red, *pw, *stage;
     Ctrl* ctrl = nullptr;
-    Ctrl* h_ctrl = nullptr;                  // pinned mirror
-    double* h_scal = nullptr;                // pinned scalars
-    unsigned long long* d_dev = nullptr;     // Ruiz deviation accumulator
+    Ctrl* h_ctrl = nullptr;
+    double* h_scal = nullptr;
+    unsigned long long* d_dev = nullptr;
     LogRec* log = nullptr;
     long long log_cap = 0;
     void* ws = nullptr;
@@ -585,117 +202,93 @@ struct hpr_handle {
     size_t ws_bytes = 0;
     long long launches = 0;
     std::vector<LogRec> h_log;
-    cudaEvent_t ev[4];
-    // cached loop graph (kernel arguments are fixed per handle, so one
-    // instantiation serves every solve with the same block size and dtype)
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // cached loop graph (kernel arguments are fixed per handle)
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
     unsigned long long gcond = 0;
     int g_B = 0, g_prec = -1;
     long long g_per_block = 0;
-    int last_prec = -1;          // precision of the last solve (-1: none)
-    // locality ordering (new -> old); identity when reorder is off
+    int last_prec = -1;
     bool reordered = false;
     int *rperm = nullptr, *cperm = nullptr;
-    double* stage = nullptr;     // max(m, n) staging for permuted I/O
-    double* SP = nullptr;        // max(m, n) product vector of the split (unfused) iteration
-    bool fuse = false;           // epilogue fused into the SpMV (HPR_FUSE=1) or separate pass
 };
 
 namespace {
 
 constexpr long long LOG_CAP_MAX = 1 << 20;
 
-struct Layout {
-    size_t bytes;
-};
-
-// Upper bounds on the tile schedule of a CSR with `rows` rows and `nnz`
-// nonzeros, independent of the row order (so the workspace can be sized
-// before the locality ordering is computed).  A stream tile closes on a
-// full row count, on nnz overflow (two consecutive tiles then hold more than
-// TILE_NNZ), before a long row, or at the end.
-struct TileBound {
-    size_t tiles, longs;
-};
-TileBound tile_bound(long long rows, long long nnz) {
-    const long long nlong = std::min<long long>(rows, nnz / (TILE_NNZ + 1));
-    const long long t = 2 * (nnz / TILE_NNZ + 1) + rows / TILE_ROWS + 1 + 2 * nlong +
-                        (nnz / CHUNK_NNZ + 1) + nlong + 2;
-    return {(size_t)t, (size_t)std::max<long long>(nlong, 1)};
-}
-
 // Carve every device array from one block; base == nullptr only measures.
+// Folded operands are sized for the unfolded worst case.
 size_t carve(hpr_handle* h, char* base) {
-    const TileBound ba = tile_bound(h->m, h->nnz), bt = tile_bound(h->n, h->nnz);
-    struct {
-        size_t tiles, longs;
-    } pa_{ba.tiles, ba.longs}, pt_{bt.tiles, bt.longs};
     Carver cv;
     cv.base = base;
     const size_t m = h->m, n = h->n, nnz = h->nnz;
-    h->A.ptr = cv.take<int>(m + 1);
-    h->A.idx = cv.take<int>(nnz);
-    h->A.mval = cv.take<double>(nnz);
-    h->A.w64 = cv.take<double>(nnz);
-    h->A.w32 = cv.take<float>(nnz);
-    h->AT.ptr = cv.take<int>(n + 1);
-    h->AT.idx = cv.take<int>(nnz);
-    h->AT.mval = cv.take<double>(nnz);
-    h->AT.w64 = cv.take<double>(nnz);
-    h->AT.w32 = cv.take<float>(nnz);
-    h->A.tiles = cv.take<int4>(pa_.tiles);
-    h->A.longs = cv.take<int4>(pa_.longs);
-    h->A.counters = cv.take<int>(pa_.longs);
-    h->A.tpart = cv.take<double>(pa_.tiles);
-    h->AT.tiles = cv.take<int4>(pt_.tiles);
-    h->AT.longs = cv.take<int4>(pt_.longs);
-    h->AT.counters = cv.take<int>(pt_.longs);
-    h->AT.tpart = cv.take<double>(pt_.tiles);
-    h->rhs_m = cv.take<double>(m);
-    h->cost_m = cv.take<double>(n);
-    h->lo_m = cv.take<double>(n);
-    h->up_m = cv.take<double>(n);
-    h->rs = cv.take<double>(m);
-    h->cs = cv.take<double>(n);
-    h->fr = cv.take<double>(m);
-    h->fc = cv.take<double>(n);
-    h->rhs_w = cv.take<double>(m);
-    h->cost_w = cv.take<double>(n);
-    h->lo_w = cv.take<double>(n);
-    h->up_w = cv.take<double>(n);
-    h->rhsT = cv.take<double>(m);
-    h->costT = cv.take<double>(n);
-    h->loT = cv.take<double>(n);
-    h->upT = cv.take<double>(n);
-    h->X = cv.take<double>(n);
-    h->Z = cv.take<double>(n);
-    h->AXv = cv.take<double>(n);
-    h->AZv = cv.take<double>(n);
-    h->XT = cv.take<double>(n);
-    h->BX = cv.take<double>(n);
-    h->BZ = cv.take<double>(n);
-    h->Y = cv.take<double>(m);
-    h->AYv = cv.take<double>(m);
-    h->BY = cv.take<double>(m);
-    h->XM = cv.take<double>(n);
-    h->ZM = cv.take<double>(n);
-    h->YM = cv.take<double>(m);
-    h->BXm = cv.take<double>(n);
-    h->BZm = cv.take<double>(n);
-    h->BYm = cv.take<double>(m);
-    const size_t nsa = pa_.tiles + pa_.longs, nst = pt_.tiles + pt_.longs;
-    h->rowpart = cv.take<double>(KR * nsa);
-    h->colpart = cv.take<double>(KC * std::max(nst, nsa));
+    const TileBound bm = tile_bound(m, nnz), bn = tile_bound(n, nnz);
+    auto csr = [&](DevCsr& M, size_t rows, const TileBound& tb, bool work32, bool src) {
+        M.ptr = cv.take<int>(rows + 1);
+        M.idx = cv.take<int>(nnz);
+        M.mval = cv.take<double>(nnz);
+        M.w64 = cv.take<double>(nnz);
+        M.w32 = work32 ? cv.take<float>(nnz) : nullptr;
+        M.src = src ? cv.take<int>(nnz) : nullptr;
+        M.tiles = cv.take<int4>(tb.tiles);
+        M.longs = cv.take<int4>(tb.longs);
+        M.counters = cv.take<int>(tb.longs);
+        M.tpart = cv.take<double>(tb.tiles);
+    };
+    csr(h->A, m, bm, false, false);
+    csr(h->AT, n, bn, false, false);
+    csr(h->F, m, bm, true, true);
+    csr(h->FT, n, bn, true, true);
+    h->frow = cv.take<int>(m + 1);
+    for (double** v : {&h->rhs_m, &h->rs, &h->fr, &h->rhs_w, &h->YM, &h->YMF, &h->BYm})
+        *v = cv.take<double>(m);
+    for (double** v : {&h->cost_m, &h->lo_m, &h->up_m, &h->cs, &h->fc, &h->cost_w, &h->lo_w,
+                       &h->up_w, &h->XM, &h->ZM, &h->BXm, &h->BZm})
+        *v = cv.take<double>(n);
+    for (void** v : {&h->rhsT, &h->Y, &h->AYv, &h->BY, &h->YF, &h->BYF}) *v = cv.take<double>(m);
+    for (void** v : {&h->costT, &h->loT, &h->upT, &h->X, &h->Z, &h->AXv, &h->AZv, &h->XT,
+                     &h->BX, &h->BZ})
+        *v = cv.take<double>(n);
+    h->P = cv.take<double>(std::max(m, n));
+    const size_t nslot = std::max({bm.tiles + bm.longs, bn.tiles + bn.longs, (size_t)ROW_GRID_MAX});
+    h->rowpart = cv.take<double>(KR * nslot);
+    h->colpart = cv.take<double>(KC * nslot);
     h->red = cv.take<double>(RED_BLOCKS + 64);
     h->pw = cv.take<double>(m + n);
+    h->stage = cv.take<double>(std::max(m, n));
     h->rperm = cv.take<int>(m);
     h->cperm = cv.take<int>(n);
-    h->stage = cv.take<double>(std::max(m, n));
-    h->SP = cv.take<double>(std::max(m, n));
     h->ctrl = cv.take<Ctrl>(1);
     h->d_dev = cv.take<unsigned long long>(2);
     return cv.off + 256;
+}
+
+// ===========================================================================
+// host-side layout: transpose, locality ordering, twin folding
+// ===========================================================================
+
+struct HostCsr {
+    std::vector<int32_t> ptr, idx;
+    std::vector<double> val;
+    std::vector<int32_t> src;    // only for folded operands
+};
+
+void host_transpose(int m, int n, const HostCsr& a, HostCsr& t) {
+    const long long nnz = a.ptr[m];
+    t.ptr.assign(n + 1, 0);
+    for (long long e = 0; e < nnz; ++e) t.ptr[a.idx[e] + 1]++;
+    for (int j = 0; j < n; ++j) t.ptr[j + 1] += t.ptr[j];
+    std::vector<int32_t> next(t.ptr.begin(), t.ptr.end() - 1);
+    t.idx.resize(nnz);
+    t.val.resize(nnz);
+    for (int i = 0; i < m; ++i)
+        for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e) {
+            const int p = next[a.idx[e]]++;
+            t.idx[p] = i;
+            t.val[p] = a.val[e];
+        }
 }
 
 // Locality ordering (SURVEY.md §7 hard part 5).  The reference lays
@@ -708,76 +301,103 @@ size_t carve(hpr_handle* h, char* base) {
 // keeps the reference's summation order; only the labels move.
 constexpr int LONG_ROW = 256;
 
-void compute_order(int m, int n, int n_eq, const std::vector<int32_t>& ptr,
-                   const std::vector<int32_t>& idx, std::vector<int32_t>& rperm,
+void compute_order(int m, int n, int n_eq, const HostCsr& a, std::vector<int32_t>& rperm,
                    std::vector<int32_t>& cperm) {
     const int INF = 0x7fffffff;
     std::vector<int32_t> ckey(n, INF);
     for (int i = 0; i < m; ++i)
-        if (ptr[i + 1] - ptr[i] > LONG_ROW)
-            for (int e = ptr[i]; e < ptr[i + 1]; ++e)
-                if (ckey[idx[e]] == INF) ckey[idx[e]] = i;
+        if (a.ptr[i + 1] - a.ptr[i] > LONG_ROW)
+            for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e)
+                if (ckey[a.idx[e]] == INF) ckey[a.idx[e]] = i;
     cperm.resize(n);
     for (int j = 0; j < n; ++j) cperm[j] = j;
-    std::stable_sort(cperm.begin(), cperm.end(),
-                     [&](int a, int b) { return ckey[a] < ckey[b]; });
+    std::stable_sort(cperm.begin(), cperm.end(), [&](int x, int y) { return ckey[x] < ckey[y]; });
     std::vector<int32_t> cinv(n);
     for (int k = 0; k < n; ++k) cinv[cperm[k]] = k;
     std::vector<int32_t> rkey(m, INF);
     for (int i = 0; i < m; ++i)
-        for (int e = ptr[i]; e < ptr[i + 1]; ++e) rkey[i] = std::min(rkey[i], cinv[idx[e]]);
+        for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e) rkey[i] = std::min(rkey[i], cinv[a.idx[e]]);
     rperm.resize(m);
     for (int i = 0; i < m; ++i) rperm[i] = i;
-    auto by = [&](int a, int b) { return rkey[a] < rkey[b]; };
+    auto by = [&](int x, int y) { return rkey[x] < rkey[y]; };
     std::stable_sort(rperm.begin(), rperm.begin() + n_eq, by);
     std::stable_sort(rperm.begin() + n_eq, rperm.end(), by);
 }
 
-// relabel a CSR: new row r' = old row perm_rows[r'], columns through inv_cols
-void permute_csr(int rows, const std::vector<int32_t>& ptr, const std::vector<int32_t>& idx,
-                 const std::vector<double>& val, const std::vector<int32_t>& perm_rows,
-                 const std::vector<int32_t>& inv_cols, std::vector<int32_t>& nptr,
-                 std::vector<int32_t>& nidx, std::vector<double>& nval) {
-    nptr.assign(rows + 1, 0);
-    for (int r = 0; r < rows; ++r) nptr[r + 1] = nptr[r] + (ptr[perm_rows[r] + 1] - ptr[perm_rows[r]]);
-    nidx.resize(idx.size());
-    nval.resize(val.size());
+// relabel: new row r' = old row perm_rows[r'], columns through inv_cols
+void permute_csr(int rows, const HostCsr& a, const std::vector<int32_t>& perm_rows,
+                 const std::vector<int32_t>& inv_cols, HostCsr& out) {
+    out.ptr.assign(rows + 1, 0);
+    for (int r = 0; r < rows; ++r)
+        out.ptr[r + 1] = out.ptr[r] + (a.ptr[perm_rows[r] + 1] - a.ptr[perm_rows[r]]);
+    out.idx.resize(a.idx.size());
+    out.val.resize(a.val.size());
     for (int r = 0; r < rows; ++r) {
-        const int o = perm_rows[r];
-        int q = nptr[r];
-        for (int e = ptr[o]; e < ptr[o + 1]; ++e, ++q) {
-            nidx[q] = inv_cols[idx[e]];
-            nval[q] = val[e];
+        int q = out.ptr[r];
+        for (int e = a.ptr[perm_rows[r]]; e < a.ptr[perm_rows[r] + 1]; ++e, ++q) {
+            out.idx[q] = inv_cols[a.idx[e]];
+            out.val[q] = a.val[e];
         }
     }
 }
 
-__global__ void k_gather(double* dst, const double* src, const int* perm, int len) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < len) dst[i] = src[perm[i]];
-}
-
-__global__ void k_scatter(double* dst, const double* src, const int* perm, int len) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < len) dst[perm[i]] = src[i];
-}
-
-void host_transpose(int m, int n, const int32_t* ptr, const int32_t* idx, const double* val,
-                    std::vector<int32_t>& tptr, std::vector<int32_t>& tidx,
-                    std::vector<double>& tval) {
-    const long long nnz = ptr[m];
-    tptr.assign(n + 1, 0);
-    for (long long e = 0; e < nnz; ++e) tptr[idx[e] + 1]++;
-    for (int j = 0; j < n; ++j) tptr[j + 1] += tptr[j];
-    std::vector<int32_t> next(tptr.begin(), tptr.end() - 1);
-    tidx.resize(nnz);
-    tval.resize(nnz);
-    for (int i = 0; i < m; ++i)
-        for (int e = ptr[i]; e < ptr[i + 1]; ++e) {
-            const int p = next[idx[e]]++;
-            tidx[p] = i;
-            tval[p] = val[e];
+// Twin folding (hpr_update.cuh): consecutive inequality rows with the same
+// pattern and exactly negated coefficients are stored once.
+void fold_twins(int m, int n, int n_eq, const HostCsr& a, const HostCsr& at,
+                std::vector<int32_t>& frow, HostCsr& f, HostCsr& ft) {
+    std::vector<int32_t> fold_of(m), second(m, 0);
+    frow.clear();
+    for (int i = 0; i < m;) {
+        bool pair = false;
+        if (i >= n_eq && i + 1 < m) {
+            const int b0 = a.ptr[i], l0 = a.ptr[i + 1] - b0;
+            const int b1 = a.ptr[i + 1], l1 = a.ptr[i + 2] - b1;
+            if (l0 == l1 && l0 > 0) {
+                pair = true;
+                for (int k = 0; k < l0 && pair; ++k)
+                    pair = a.idx[b0 + k] == a.idx[b1 + k] && a.val[b1 + k] == -a.val[b0 + k];
+            }
         }
+        fold_of[i] = (int)frow.size();
+        if (pair) {
+            fold_of[i + 1] = (int)frow.size();
+            second[i + 1] = 1;
+        }
+        frow.push_back(i);
+        i += pair ? 2 : 1;
+    }
+    const int nf = (int)frow.size();
+    frow.push_back(m);
+    f.ptr.assign(nf + 1, 0);
+    for (int q = 0; q < nf; ++q) f.ptr[q + 1] = f.ptr[q] + (a.ptr[frow[q] + 1] - a.ptr[frow[q]]);
+    f.idx.resize(f.ptr[nf]);
+    f.val.resize(f.ptr[nf]);
+    f.src.resize(f.ptr[nf]);
+    for (int q = 0; q < nf; ++q) {
+        int o = f.ptr[q];
+        for (int e = a.ptr[frow[q]]; e < a.ptr[frow[q] + 1]; ++e, ++o) {
+            f.idx[o] = a.idx[e];
+            f.val[o] = a.val[e];
+            f.src[o] = e;
+        }
+    }
+    ft.ptr.assign(n + 1, 0);
+    ft.idx.clear();
+    ft.val.clear();
+    ft.src.clear();
+    ft.idx.reserve(f.idx.size());
+    ft.val.reserve(f.idx.size());
+    ft.src.reserve(f.idx.size());
+    for (int j = 0; j < n; ++j) {
+        for (int e = at.ptr[j]; e < at.ptr[j + 1]; ++e) {
+            const int i = at.idx[e];
+            if (second[i]) continue;
+            ft.idx.push_back(fold_of[i]);
+            ft.val.push_back(at.val[e]);
+            ft.src.push_back(e);
+        }
+        ft.ptr[j + 1] = (int32_t)ft.idx.size();
+    }
 }
 
 template <typename T>
@@ -794,8 +414,6 @@ std::vector<T> to_host(const T* p, size_t count) {
     }
     return v;
 }
-
-inline int nblk(long long n, int tpb = TPB) { return (int)std::max<long long>(1, (n + tpb - 1) / tpb); }
 
 // caller vector (original order, host or device) -> device vector (engine order)
 void put_vec(hpr_handle* h, double* dst, const double* src, int len, bool rows) {
@@ -829,7 +447,7 @@ void validate(const hpr_problem* p) {
     if (!p->rhs || !p->cost || !p->lower || !p->upper) fail(HPR_ERR_INVALID, "LP vectors missing");
 }
 
-// deterministic ||v||^2 on device -> host
+// deterministic ||v||^2 on the device -> host
 double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only) {
     k_sumsq_part<<<RED_BLOCKS, TPB, 0, h->stream>>>(v, n, finite_only, h->red);
     CKL();
@@ -845,23 +463,12 @@ double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only) {
 template <typename T, class Epi>
 void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, const Epi& epi,
                  cudaStream_t s) {
-    if (M.pipe) {
-        static bool attr_set = false;   // one per template instantiation
-        constexpr size_t smem = pipe_smem_bytes<T>();
-        if (!attr_set) {
-            CK(cudaFuncSetAttribute(k_spmv_pipe<T, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-            attr_set = true;
-        }
-        k_spmv_pipe<T, Epi><<<M.nblocks, TPB, smem, s>>>(M.view<T>(vals), xg, epi);
-    } else {
-        k_spmv<T, Epi><<<M.ntiles, TPB, 0, s>>>(M.view<T>(vals), xg, epi);
-    }
+    k_spmv<T, Epi><<<M.ntiles, TPB, 0, s>>>(M.view<T>(vals), xg, epi);
     CKL();
     h->launches += 1;
 }
 
-// power_method (lp_kernel.py:138-175) on an FP64 operand pair (A, A^T)
+// power_method (lp_kernel.py:138-175) on the unfolded FP64 operand pair
 double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, double tol,
                     int max_iter, double inflation, const double* start, int start_count,
                     int* iters_out, int* conv_out) {
@@ -915,7 +522,29 @@ double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, 
     return lam * inflation;
 }
 
-// Ruiz -> Pock-Chambolle -> normalisation on device (hprlp.py:213-264)
+// copy the scaled unfolded values into the folded operands
+void refresh_folded_values(hpr_handle* h, bool fp32) {
+    cudaStream_t s = h->stream;
+    if (h->folded) {
+        k_gather_vals<<<nblk(h->nnz_f), TPB, 0, s>>>(h->F.w64, h->A.w64, h->F.src, h->nnz_f);
+        k_gather_vals<<<nblk(h->nnz_f), TPB, 0, s>>>(h->FT.w64, h->AT.w64, h->FT.src, h->nnz_f);
+        CKL();
+        h->launches += 2;
+    } else {
+        CK(cudaMemcpyAsync(h->F.w64, h->A.w64, sizeof(double) * h->nnz, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(h->FT.w64, h->AT.w64, sizeof(double) * h->nnz, cudaMemcpyDeviceToDevice, s));
+    }
+    if (fp32) {
+        k_cast_f32<<<nblk(h->nnz_f), TPB, 0, s>>>(h->F.w64, h->F.w32, h->nnz_f);
+        k_cast_f32<<<nblk(h->nnz_f), TPB, 0, s>>>(h->FT.w64, h->FT.w32, h->nnz_f);
+        CKL();
+        h->launches += 2;
+    }
+}
+
+// Ruiz -> Pock-Chambolle -> normalisation on device (hprlp.py:213-264), on
+// the unfolded operands so every norm sums the same terms in the same order
+// as the reference.
 void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double* csc_out) {
     cudaStream_t s = h->stream;
     const int m = h->m, n = h->n;
@@ -945,8 +574,7 @@ void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double
             apply();
             CK(cudaMemcpyAsync(h->h_scal, h->d_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            const double d = std::max(h->h_scal[0], h->h_scal[1]);
-            if (d < 1e-6) break;
+            if (std::max(h->h_scal[0], h->h_scal[1]) < 1e-6) break;
         }
     }
     if (prm->pock_chambolle) {
@@ -978,12 +606,13 @@ void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double
 
 template <typename T>
 struct Ptrs {
-    T *X, *Y, *Z, *AX, *AY, *AZ, *XT, *BX, *BY, *BZ;
-    const T *rhs, *cost, *lo, *up, *a_vals, *at_vals;
+    T *X, *Y, *Z, *AX, *AY, *AZ, *XT, *BX, *BY, *BZ, *YF, *BYF, *P;
+    const T *rhs, *cost, *lo, *up, *f_vals, *ft_vals;
 };
 
 template <typename T>
-Ptrs<T> ptrs(hpr_handle* h, bool fp32) {
+Ptrs<T> ptrs(hpr_handle* h) {
+    const bool fp32 = sizeof(T) == 4;
     Ptrs<T> p;
     p.X = (T*)h->X;
     p.Y = (T*)h->Y;
@@ -995,96 +624,64 @@ Ptrs<T> ptrs(hpr_handle* h, bool fp32) {
     p.BX = (T*)h->BX;
     p.BY = (T*)h->BY;
     p.BZ = (T*)h->BZ;
-    if (fp32) {
-        p.rhs = (const T*)h->rhsT;
-        p.cost = (const T*)h->costT;
-        p.lo = (const T*)h->loT;
-        p.up = (const T*)h->upT;
-        p.a_vals = (const T*)h->A.w32;
-        p.at_vals = (const T*)h->AT.w32;
-    } else {
-        p.rhs = (const T*)h->rhs_w;
-        p.cost = (const T*)h->cost_w;
-        p.lo = (const T*)h->lo_w;
-        p.up = (const T*)h->up_w;
-        p.a_vals = (const T*)h->A.w64;
-        p.at_vals = (const T*)h->AT.w64;
-    }
+    p.YF = (T*)h->YF;
+    p.BYF = (T*)h->BYF;
+    p.P = (T*)h->P;
+    p.rhs = (const T*)(fp32 ? h->rhsT : (void*)h->rhs_w);
+    p.cost = (const T*)(fp32 ? h->costT : (void*)h->cost_w);
+    p.lo = (const T*)(fp32 ? h->loT : (void*)h->lo_w);
+    p.up = (const T*)(fp32 ? h->upT : (void*)h->up_w);
+    p.f_vals = (const T*)(fp32 ? (void*)h->F.w32 : (void*)h->F.w64);
+    p.ft_vals = (const T*)(fp32 ? (void*)h->FT.w32 : (void*)h->FT.w64);
     return p;
 }
 
-// the check phase: master-space residual of the bar triple + controller + copies
+// KKT residual of the master bar triple (XM, YM(F), ZM) + controller + copies
 template <typename T>
 void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
-    EpiCheckRows<T> er{h->n_eq, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
-    launch_spmv(h, h->A, (const double*)h->A.mval, (const double*)h->XM, er, s);
-    EpiCheckCols<T> ec{h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX, h->colpart};
-    launch_spmv(h, h->AT, (const double*)h->AT.mval, (const double*)h->YM, ec, s);
-    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, h->A.nslots(), h->colpart,
-                                        h->AT.nslots(), h->log, mode);
+    double* pd = (double*)h->P;
+    EpiStore<double> st{pd, nullptr};
+    launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
+    const int gr = row_grid(h->nf), gc = row_grid(h->n);
+    CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
+    k_check_rows<T><<<gr, TPB, 0, s>>>(ar);
+    CKL();
+    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
+                        h->colpart};
+    k_check_cols<T><<<gc, TPB, 0, s>>>(ac);
+    CKL();
+    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, gr, h->colpart, gc, h->log, mode);
     CKL();
     const int len = std::max(h->n, h->m);
-    k_restart_copy<T><<<std::min(nblk(len), 148 * 8), TPB, 0, s>>>(
-        h->ctrl, h->n, h->m, h->XM, h->YM, h->ZM, h->BXm, h->BYm, h->BZm, p.X, p.Y, p.Z, p.AX,
-        p.AY, p.AZ, p.BX, p.BY, p.BZ);
+    k_restart_copy<T><<<row_grid(len), TPB, 0, s>>>(h->ctrl, h->n, h->m, h->nf, h->XM, h->YM,
+                                                    h->ZM, h->BXm, h->BYm, h->BZm, p.X, p.Y, p.Z,
+                                                    p.AX, p.AY, p.AZ, p.BX, p.BY, p.BZ, p.YF,
+                                                    p.BYF);
+    CKL();
+    h->launches += 4;
+}
+
+template <typename T, bool CHECK>
+void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
+    EpiStore<T> st{p.P, nullptr};
+    launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s);                       // A^T y
+    PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
+                     p.BX, p.BZ, h->XM, h->ZM, h->cs};
+    k_update_primal<T, CHECK><<<row_grid(h->n), TPB, 0, s>>>(pa);
+    CKL();
+    launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s);                         // A x~
+    DualArgs<T> da{h->ctrl, j, h->nf, h->n_eq, h->frow, p.P, p.Y, p.AY, p.rhs, p.YF,
+                   p.BY, p.BYF, h->YM, h->YMF, h->rs};
+    k_update_dual<T, CHECK><<<row_grid(h->nf), TPB, 0, s>>>(da);
     CKL();
     h->launches += 2;
 }
 
-// One row-wise pass of an epilogue over a precomputed product vector:
-// the projection / reflection / Halpern update of a whole half-iteration in
-// one coalesced sweep (the split form of the fused SpMV epilogue).
-template <typename T, class Epi>
-__global__ void __launch_bounds__(TPB) k_rowwise(Epi epi, const T* __restrict__ sums, int len) {
-    epi.prepare();
-    Acc<0> acc;
-    for (int j = blockIdx.x * TPB + threadIdx.x; j < len; j += gridDim.x * TPB) {
-        typename Epi::Pre pre;
-        epi.load(j, pre);
-        epi.apply(j, sums[j], pre, acc);
-    }
-}
-
-template <typename T, class Epi>
-void launch_rowwise(hpr_handle* h, const Epi& epi, const T* sums, int len, cudaStream_t s) {
-    k_rowwise<T, Epi><<<std::min(nblk(len), 148 * 16), TPB, 0, s>>>(epi, sums, len);
-    CKL();
-    h->launches += 1;
-}
-
-template <typename T, bool CHECK>
-void enqueue_split(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
-    T* sp = (T*)h->SP;
-    EpiStore<T> st{sp, nullptr};
-    launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, st, s);
-    EpiPrimal<T, CHECK> e1{h->ctrl, j, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                           p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
-    launch_rowwise(h, e1, (const T*)sp, h->n, s);
-    launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, st, s);
-    EpiDual<T, CHECK> e2{h->ctrl, j, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
-    launch_rowwise(h, e2, (const T*)sp, h->m, s);
-}
-
 template <typename T>
 void enqueue_iteration(hpr_handle* h, const Ptrs<T>& p, int j, bool check, cudaStream_t s) {
-    if (!h->fuse) {
-        if (check) enqueue_split<T, true>(h, p, j, s);
-        else enqueue_split<T, false>(h, p, j, s);
-        return;
-    }
-    if (check) {
-        EpiPrimal<T, true> e1{h->ctrl, j, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                              p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
-        launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s);
-        EpiDual<T, true> e2{h->ctrl, j, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
-        launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s);
-    } else {
-        EpiPrimal<T, false> e1{h->ctrl, j, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                               p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
-        launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s);
-        EpiDual<T, false> e2{h->ctrl, j, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
-        launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s);
-    }
+    if (check) enqueue_iteration_t<T, true>(h, p, j, s);
+    else enqueue_iteration_t<T, false>(h, p, j, s);
 }
 
 template <typename T>
@@ -1095,7 +692,7 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     if (h->graph) cudaGraphDestroy(h->graph);
     h->gexec = nullptr;
     h->graph = nullptr;
-    // WHILE(cond) { B fused iterations; master check; controller; copies }
+    // WHILE(cond) { B iterations; master check; controller; copies }
     CK(cudaGraphCreate(&h->graph, 0));
     cudaGraphConditionalHandle cond;
     CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
@@ -1147,6 +744,17 @@ void read_ctrl(hpr_handle* h) {
     CK(cudaStreamSynchronize(h->stream));
 }
 
+void cast_work_vectors(hpr_handle* h) {
+    cudaStream_t s = h->stream;
+    const int m = h->m, n = h->n;
+    k_cast_f32<<<nblk(m), TPB, 0, s>>>(h->rhs_w, (float*)h->rhsT, m);
+    k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->cost_w, (float*)h->costT, n);
+    k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->lo_w, (float*)h->loT, n);
+    k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->up_w, (float*)h->upT, n);
+    CKL();
+    h->launches += 4;
+}
+
 template <typename T>
 void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const double* y0,
                  const double* z0, double* xo, double* yo, double* zo, hpr_stats* st,
@@ -1158,7 +766,6 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
 
     double bsc, csc;
     scale_problem(h, prm, &bsc, &csc);
-
     int pits = 0, pconv = 0;
     const double lam = power_method(h, h->A.w64, h->AT.w64, prm->power_tol, prm->power_max_iter,
                                     prm->power_inflation, prm->power_start,
@@ -1171,19 +778,10 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     else sigma = 1.0;
     const double rhs_norm_m = std::sqrt(dev_sumsq(h, h->rhs_m, m, 0));
     const double cost_norm_m = std::sqrt(dev_sumsq(h, h->cost_m, n, 0));
+    refresh_folded_values(h, fp32);
+    if (fp32) cast_work_vectors(h);
 
-    if (fp32) {
-        k_cast_f32<<<nblk(h->nnz), TPB, 0, s>>>(h->A.w64, h->A.w32, h->nnz);
-        k_cast_f32<<<nblk(h->nnz), TPB, 0, s>>>(h->AT.w64, h->AT.w32, h->nnz);
-        k_cast_f32<<<nblk(m), TPB, 0, s>>>(h->rhs_w, (float*)h->rhsT, m);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->cost_w, (float*)h->costT, n);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->lo_w, (float*)h->loT, n);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->up_w, (float*)h->upT, n);
-        CKL();
-        h->launches += 6;
-    }
-
-    // device-resident warm start (master space)
+    // initial point (hprlp.py:357-365), warm start given in master space
     const double *dx0 = nullptr, *dy0 = nullptr, *dz0 = nullptr;
     if (x0 && y0 && z0) {
         put_vec(h, h->BXm, x0, n, false);
@@ -1193,12 +791,14 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
         dy0 = h->BYm;
         dz0 = h->BZm;
     }
-    Ptrs<T> p = ptrs<T>(h, fp32);
+    Ptrs<T> p = ptrs<T>(h);
     k_init_cols<T><<<nblk(n), TPB, 0, s>>>(n, dx0, dz0, h->cs, bsc, csc, h->lo_w, h->up_w, p.X,
                                            p.Z, p.AX, p.AZ, p.BX, p.BZ, h->XM, h->ZM);
     k_init_rows<T><<<nblk(m), TPB, 0, s>>>(m, dy0, h->rs, csc, p.Y, p.AY, p.BY, h->YM);
+    k_fold_rows<T><<<nblk(h->nf), TPB, 0, s>>>(h->nf, h->frow, p.Y, p.YF, p.BY, p.BYF, h->YM,
+                                                h->YMF);
     CKL();
-    h->launches += 2;
+    h->launches += 3;
 
     const int B = prm->log_every_iteration ? 1 : std::max(1, prm->check_every);
     if (B > MAX_B) fail(HPR_ERR_INVALID, "check_every too large");
@@ -1248,6 +848,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
             iterations = prm->max_iterations;
         }
     }
+    st->loop_seconds = 0.0;
     if (status == -1) {
         if (prm->time_limit >= 0) {
             const double rem = std::max(0.0, prm->time_limit - elapsed);
@@ -1262,8 +863,6 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
         status = h->h_ctrl->status;
         iterations = h->h_ctrl->total;
         if (status == HPR_ITERATION_LIMIT) iterations = prm->max_iterations;
-    } else {
-        st->loop_seconds = 0.0;
     }
     float sms = 0.f;
     CK(cudaEventElapsedTime(&sms, h->ev[0], h->ev[1]));
@@ -1296,7 +895,35 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     CK(cudaStreamSynchronize(s));
 }
 
-Plan plan_for(const int32_t* ptr, int rows) { return build_tiles(ptr, rows); }
+void upload_csr(hpr_handle* h, DevCsr& M, const HostCsr& c, int rows, int cols, const Plan& pl,
+                bool with_src) {
+    cudaStream_t s = h->stream;
+    M.rows = rows;
+    M.cols = cols;
+    M.nnz = c.idx.size();
+    M.ntiles = (int)pl.tiles.size();
+    M.nlong = (int)pl.longs.size();
+    CK(cudaMemcpyAsync(M.ptr, c.ptr.data(), sizeof(int) * (rows + 1), cudaMemcpyHostToDevice, s));
+    if (M.nnz) {
+        CK(cudaMemcpyAsync(M.idx, c.idx.data(), sizeof(int) * M.nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(M.mval, c.val.data(), sizeof(double) * M.nnz, cudaMemcpyHostToDevice, s));
+        if (with_src)
+            CK(cudaMemcpyAsync(M.src, c.src.data(), sizeof(int) * M.nnz, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemcpyAsync(M.tiles, pl.tiles.data(), sizeof(int4) * pl.tiles.size(), cudaMemcpyHostToDevice, s));
+    if (!pl.longs.empty()) {
+        CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
+    }
+    // the host buffers must outlive the async copies
+    CK(cudaStreamSynchronize(s));
+}
+
+void check_plan(const Plan& p, long long rows, long long nnz) {
+    const TileBound b = tile_bound(rows, nnz);
+    if (p.tiles.size() > b.tiles || p.longs.size() > b.longs)
+        fail(HPR_ERR_INVALID, "internal: tile bound violated");
+}
 
 }  // namespace
 
@@ -1334,6 +961,8 @@ int hpr_workspace_bytes(const hpr_problem* p, size_t* bytes) {
     API_END
 }
 
+void hpr_destroy(hpr_handle* h);
+
 int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
     hpr_handle* h = nullptr;
     try {
@@ -1347,49 +976,62 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         h->n_eq = p->n_eq;
         h->nnz = p->nnz;
         h->offset = p->offset;
-        std::vector<int32_t> ptr = to_host(p->indptr, (size_t)p->m + 1);
-        if (ptr[0] != 0 || ptr[p->m] != p->nnz) fail(HPR_ERR_INVALID, "indptr inconsistent with nnz");
-        std::vector<int32_t> idx = to_host(p->indices, (size_t)p->nnz);
-        std::vector<double> val = to_host(p->data, (size_t)p->nnz);
-        for (int i = 0; i < p->m; ++i)
-            if (ptr[i + 1] < ptr[i]) fail(HPR_ERR_INVALID, "indptr not monotone");
-        for (auto c : idx)
-            if (c < 0 || c >= p->n) fail(HPR_ERR_INVALID, "column index out of range");
-        std::vector<int32_t> tptr, tidx;
-        std::vector<double> tval;
+        const int m = p->m, n = p->n;
+        HostCsr a;
+        a.ptr = to_host(p->indptr, (size_t)m + 1);
+        if (a.ptr[0] != 0 || a.ptr[m] != p->nnz) fail(HPR_ERR_INVALID, "indptr inconsistent with nnz");
+        a.idx = to_host(p->indices, (size_t)p->nnz);
+        a.val = to_host(p->data, (size_t)p->nnz);
+        for (int i = 0; i < m; ++i)
+            if (a.ptr[i + 1] < a.ptr[i]) fail(HPR_ERR_INVALID, "indptr not monotone");
+        for (auto c : a.idx)
+            if (c < 0 || c >= n) fail(HPR_ERR_INVALID, "column index out of range");
+        HostCsr at;
         if (p->t_indptr && p->t_indices && p->t_data) {
-            tptr = to_host(p->t_indptr, (size_t)p->n + 1);
-            tidx = to_host(p->t_indices, (size_t)p->nnz);
-            tval = to_host(p->t_data, (size_t)p->nnz);
+            at.ptr = to_host(p->t_indptr, (size_t)n + 1);
+            at.idx = to_host(p->t_indices, (size_t)p->nnz);
+            at.val = to_host(p->t_data, (size_t)p->nnz);
         } else {
-            host_transpose(p->m, p->n, ptr.data(), idx.data(), val.data(), tptr, tidx, tval);
+            host_transpose(m, n, a, at);
         }
+        const int flags = opt ? opt->flags : 0;
         std::vector<int32_t> rperm, cperm;
-        const bool reorder = !(opt && (opt->flags & HPR_FLAG_NO_REORDER));
-        if (reorder) {
-            compute_order(p->m, p->n, p->n_eq, ptr, idx, rperm, cperm);
-            std::vector<int32_t> rinv(p->m), cinv(p->n);
-            for (int i = 0; i < p->m; ++i) rinv[rperm[i]] = i;
-            for (int j = 0; j < p->n; ++j) cinv[cperm[j]] = j;
-            std::vector<int32_t> a, b;
-            std::vector<double> c;
-            permute_csr(p->m, ptr, idx, val, rperm, cinv, a, b, c);
-            ptr.swap(a);
-            idx.swap(b);
-            val.swap(c);
-            permute_csr(p->n, tptr, tidx, tval, cperm, rinv, a, b, c);
-            tptr.swap(a);
-            tidx.swap(b);
-            tval.swap(c);
+        if (!(flags & HPR_FLAG_NO_REORDER)) {
+            compute_order(m, n, p->n_eq, a, rperm, cperm);
+            std::vector<int32_t> rinv(m), cinv(n);
+            for (int i = 0; i < m; ++i) rinv[rperm[i]] = i;
+            for (int j = 0; j < n; ++j) cinv[cperm[j]] = j;
+            HostCsr t1, t2;
+            permute_csr(m, a, rperm, cinv, t1);
+            permute_csr(n, at, cperm, rinv, t2);
+            a.ptr.swap(t1.ptr);
+            a.idx.swap(t1.idx);
+            a.val.swap(t1.val);
+            at.ptr.swap(t2.ptr);
+            at.idx.swap(t2.idx);
+            at.val.swap(t2.val);
             h->reordered = true;
         }
-        Plan pa = plan_for(ptr.data(), p->m), pt = plan_for(tptr.data(), p->n);
-        {
-            const TileBound ba = tile_bound(p->m, p->nnz), bt = tile_bound(p->n, p->nnz);
-            if (pa.tiles.size() > ba.tiles || pt.tiles.size() > bt.tiles ||
-                pa.longs.size() > ba.longs || pt.longs.size() > bt.longs)
-                fail(HPR_ERR_INVALID, "internal: tile bound violated");
+        std::vector<int32_t> frow;
+        HostCsr f, ft;
+        if (!(flags & HPR_FLAG_NO_FOLD)) fold_twins(m, n, p->n_eq, a, at, frow, f, ft);
+        h->nf = frow.empty() ? m : (int)frow.size() - 1;
+        h->folded = h->nf < m;
+        if (!h->folded) {
+            frow.resize(m + 1);
+            for (int i = 0; i <= m; ++i) frow[i] = i;
+            f = a;
+            ft = at;
+            f.src.clear();
+            ft.src.clear();
         }
+        h->nnz_f = (long long)f.idx.size();
+        Plan pa = build_tiles(a.ptr.data(), m), pt = build_tiles(at.ptr.data(), n);
+        Plan pf = build_tiles(f.ptr.data(), h->nf), pft = build_tiles(ft.ptr.data(), n);
+        check_plan(pa, m, p->nnz);
+        check_plan(pt, n, p->nnz);
+        check_plan(pf, m, p->nnz);
+        check_plan(pft, n, p->nnz);
         const size_t need = carve(h, nullptr);
         if (opt && opt->workspace) {
             if (opt->workspace_bytes < need) fail(HPR_ERR_NOMEM, "workspace too small");
@@ -1412,46 +1054,19 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
         cudaStream_t s = h->stream;
-        h->A.rows = p->m;
-        h->A.cols = p->n;
-        h->AT.rows = p->n;
-        h->AT.cols = p->m;
-        h->A.ntiles = (int)pa.tiles.size();
-        h->A.nlong = (int)pa.longs.size();
-        h->AT.ntiles = (int)pt.tiles.size();
-        h->AT.nlong = (int)pt.longs.size();
-        {
-            int sms = 148;
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->dev));
-            const char* fz = getenv("HPR_FUSE");
-            h->fuse = fz && std::string(fz) == "1";
-            const char* mode = getenv("HPR_SPMV");
-            const bool pipe = mode && std::string(mode) == "pipe";
-            for (DevCsr* M : {&h->A, &h->AT}) {
-                M->pipe = pipe;
-                M->nblocks = std::max(1, std::min(M->ntiles, sms * PIPE_CTAS_PER_SM));
-            }
-        }
-        CK(cudaMemcpyAsync(h->A.ptr, ptr.data(), sizeof(int) * (p->m + 1), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->A.idx, idx.data(), sizeof(int) * p->nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->A.mval, val.data(), sizeof(double) * p->nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->AT.ptr, tptr.data(), sizeof(int) * (p->n + 1), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->AT.idx, tidx.data(), sizeof(int) * p->nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->AT.mval, tval.data(), sizeof(double) * p->nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->A.tiles, pa.tiles.data(), sizeof(int4) * pa.tiles.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->A.longs, pa.longs.data(), sizeof(int4) * pa.longs.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->AT.tiles, pt.tiles.data(), sizeof(int4) * pt.tiles.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(h->AT.longs, pt.longs.data(), sizeof(int4) * pt.longs.size(), cudaMemcpyHostToDevice, s));
-        if (!pa.longs.empty()) CK(cudaMemsetAsync(h->A.counters, 0, sizeof(int) * pa.longs.size(), s));
-        if (!pt.longs.empty()) CK(cudaMemsetAsync(h->AT.counters, 0, sizeof(int) * pt.longs.size(), s));
+        upload_csr(h, h->A, a, m, n, pa, false);
+        upload_csr(h, h->AT, at, n, m, pt, false);
+        upload_csr(h, h->F, f, h->nf, n, pf, h->folded);
+        upload_csr(h, h->FT, ft, n, h->nf, pft, h->folded);
+        CK(cudaMemcpyAsync(h->frow, frow.data(), sizeof(int) * frow.size(), cudaMemcpyHostToDevice, s));
         if (h->reordered) {
-            CK(cudaMemcpyAsync(h->rperm, rperm.data(), sizeof(int) * p->m, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(h->cperm, cperm.data(), sizeof(int) * p->n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(h->rperm, rperm.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(h->cperm, cperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
         }
-        put_vec(h, h->rhs_m, p->rhs, p->m, true);
-        put_vec(h, h->cost_m, p->cost, p->n, false);
-        put_vec(h, h->lo_m, p->lower, p->n, false);
-        put_vec(h, h->up_m, p->upper, p->n, false);
+        put_vec(h, h->rhs_m, p->rhs, m, true);
+        put_vec(h, h->cost_m, p->cost, n, false);
+        put_vec(h, h->lo_m, p->lower, n, false);
+        put_vec(h, h->up_m, p->upper, n, false);
         CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
         CK(cudaStreamSynchronize(s));
         *out = h;
@@ -1470,14 +1085,14 @@ void hpr_destroy(hpr_handle* h) {
     if (!h) return;
     cudaSetDevice(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->graph) cudaGraphDestroy(h->graph);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->log) cudaFree(h->log);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
     if (h->h_scal) cudaFreeHost(h->h_scal);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
-    if (h->graph) cudaGraphDestroy(h->graph);
     if (h->cap) cudaStreamDestroy(h->cap);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -1543,28 +1158,32 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     put_vec(h, h->XM, x, h->n, false);
     put_vec(h, h->YM, y, h->m, true);
     put_vec(h, h->ZM, z, h->n, false);
-    // bar/anchor terms are irrelevant here: point them at zeroed work buffers
-    CK(cudaMemsetAsync(h->BX, 0, sizeof(double) * h->n, s));
-    CK(cudaMemsetAsync(h->BZ, 0, sizeof(double) * h->n, s));
-    CK(cudaMemsetAsync(h->AXv, 0, sizeof(double) * h->n, s));
-    CK(cudaMemsetAsync(h->BY, 0, sizeof(double) * h->m, s));
-    CK(cudaMemsetAsync(h->AYv, 0, sizeof(double) * h->m, s));
+    // bar/anchor terms are irrelevant here: zero them (FP64 views)
+    for (void* v : {h->BX, h->BZ, h->AXv}) CK(cudaMemsetAsync(v, 0, sizeof(double) * h->n, s));
+    for (void* v : {h->BY, h->AYv}) CK(cudaMemsetAsync(v, 0, sizeof(double) * h->m, s));
+    k_fold_rows<double><<<nblk(h->nf), TPB, 0, s>>>(h->nf, h->frow, nullptr, nullptr, nullptr,
+                                                     nullptr, h->YM, h->YMF);
+    CKL();
     const double rn = std::sqrt(dev_sumsq(h, h->rhs_m, h->m, 0));
     const double cn = std::sqrt(dev_sumsq(h, h->cost_m, h->n, 0));
     Ctrl c{};
     c.denom = (1.0 + rn) + cn;
     c.offset = h->offset;
-    c.tol = 0.0;
     c.B = 1;
     c.status = -1;
     CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
-    Ptrs<double> p = ptrs<double>(h, false);
-    EpiCheckRows<double> er{h->n_eq, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
-    launch_spmv(h, h->A, (const double*)h->A.mval, (const double*)h->XM, er, s);
-    EpiCheckCols<double> ec{h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX, h->colpart};
-    launch_spmv(h, h->AT, (const double*)h->AT.mval, (const double*)h->YM, ec, s);
-    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, h->A.nslots(), h->colpart,
-                                        h->AT.nslots(), h->log, 0);
+    Ptrs<double> p = ptrs<double>(h);
+    double* pd = (double*)h->P;
+    EpiStore<double> st{pd, nullptr};
+    launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
+    const int gr = row_grid(h->nf), gc = row_grid(h->n);
+    CheckRowsArgs<double> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
+    k_check_rows<double><<<gr, TPB, 0, s>>>(ar);
+    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    CheckColsArgs<double> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
+                             h->colpart};
+    k_check_cols<double><<<gc, TPB, 0, s>>>(ac);
+    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, gr, h->colpart, gc, h->log, 0);
     CKL();
     read_ctrl(h);
     std::memcpy(out, h->h_ctrl->cur, sizeof(hpr_kkt));
@@ -1606,6 +1225,8 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     k_fill<<<nblk(m), TPB, 0, s>>>(h->rs, 1.0, m);
     k_fill<<<nblk(n), TPB, 0, s>>>(h->cs, 1.0, n);
     CKL();
+    refresh_folded_values(h, fp32);
+    if (fp32) cast_work_vectors(h);
     Ctrl c{};
     c.sigma = sigma;
     c.lam = lam;
@@ -1643,20 +1264,16 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
             get_vec(h, dst, (const double*)src, len, rows);
         }
     };
-    if (fp32) {
-        k_cast_f32<<<nblk(h->nnz), TPB, 0, s>>>(h->A.w64, h->A.w32, h->nnz);
-        k_cast_f32<<<nblk(h->nnz), TPB, 0, s>>>(h->AT.w64, h->AT.w32, h->nnz);
-        k_cast_f32<<<nblk(m), TPB, 0, s>>>(h->rhs_w, (float*)h->rhsT, m);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->cost_w, (float*)h->costT, n);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->lo_w, (float*)h->loT, n);
-        k_cast_f32<<<nblk(n), TPB, 0, s>>>(h->up_w, (float*)h->upT, n);
+    auto step = [&](auto tag) {
+        using T = decltype(tag);
+        Ptrs<T> p = ptrs<T>(h);
+        k_fold_rows<T><<<nblk(h->nf), TPB, 0, s>>>(h->nf, h->frow, p.Y, p.YF, nullptr, nullptr,
+                                                    nullptr, nullptr);
         CKL();
-        Ptrs<float> p = ptrs<float>(h, true);
-        enqueue_iteration<float>(h, p, 0, true, s);
-    } else {
-        Ptrs<double> p = ptrs<double>(h, false);
-        enqueue_iteration<double>(h, p, 0, true, s);
-    }
+        enqueue_iteration<T>(h, p, 0, true, s);
+    };
+    if (fp32) step(float(0));
+    else step(double(0));
     get(h->X, x_out, n, h->XM, false);
     get(h->Y, y_out, m, h->YM, true);
     get(h->Z, z_out, n, h->ZM, false);
@@ -1664,6 +1281,25 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     get(h->BY, bar_y, m, h->YM, true);
     get(h->BZ, bar_z, n, h->ZM, false);
     CK(cudaStreamSynchronize(s));
+    API_END
+}
+
+int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
+    API_BEGIN
+    if (!h || !out) fail(HPR_ERR_INVALID, "NULL argument");
+    out->m = h->m;
+    out->n = h->n;
+    out->n_eq = h->n_eq;
+    out->folded_rows = h->nf;
+    out->nnz = h->nnz;
+    out->folded_nnz = h->nnz_f;
+    out->tiles_a = h->A.ntiles;
+    out->tiles_at = h->AT.ntiles;
+    out->tiles_f = h->F.ntiles;
+    out->tiles_ft = h->FT.ntiles;
+    out->reordered = h->reordered;
+    out->folded = h->folded;
+    out->workspace_bytes = h->ws_bytes;
     API_END
 }
 
@@ -1702,26 +1338,25 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     API_BEGIN
     if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
+    if (which < 0 || which > 3) fail(HPR_ERR_INVALID, "unknown kernel");
     CK(cudaSetDevice(h->dev));
     cudaStream_t s = h->stream;
-    // which: 0 = A x~ product, 1 = A^T y product, 2 = primal row-wise update,
-    //        3 = dual row-wise update, 4 = fused A x~ + dual, 5 = fused A^T y + primal
+    // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update
     auto body = [&](auto tag) {
         using T = decltype(tag);
-        Ptrs<T> p = ptrs<T>(h, sizeof(T) == 4);
-        T* sp = (T*)h->SP;
-        EpiStore<T> st{sp, nullptr};
-        EpiDual<T, false> e2{h->ctrl, 0, h->n_eq, p.Y, p.AY, p.rhs, p.BY, h->YM, h->rs, nullptr};
-        EpiPrimal<T, false> e1{h->ctrl, 0, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                               p.BX, p.BZ, h->XM, h->ZM, h->cs, nullptr};
+        Ptrs<T> p = ptrs<T>(h);
+        EpiStore<T> st{p.P, nullptr};
+        PrimalArgs<T> pa{h->ctrl, 0, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
+                         p.BX, p.BZ, h->XM, h->ZM, h->cs};
+        DualArgs<T> da{h->ctrl, 0, h->nf, h->n_eq, h->frow, p.P, p.Y, p.AY, p.rhs, p.YF,
+                       p.BY, p.BYF, h->YM, h->YMF, h->rs};
         switch (which) {
-            case 0: launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, st, s); break;
-            case 1: launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, st, s); break;
-            case 2: launch_rowwise(h, e1, (const T*)sp, h->n, s); break;
-            case 3: launch_rowwise(h, e2, (const T*)sp, h->m, s); break;
-            case 4: launch_spmv(h, h->A, p.a_vals, (const T*)p.XT, e2, s); break;
-            default: launch_spmv(h, h->AT, p.at_vals, (const T*)p.Y, e1, s); break;
+            case 0: launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s); break;
+            case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s); break;
+            case 2: k_update_primal<T, false><<<row_grid(h->n), TPB, 0, s>>>(pa); break;
+            default: k_update_dual<T, false><<<row_grid(h->nf), TPB, 0, s>>>(da); break;
         }
+        CKL();
     };
     auto run = [&]() {
         if (h->last_prec == HPR_FP32) body(float(0));

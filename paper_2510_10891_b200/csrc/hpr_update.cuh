@@ -1,0 +1,204 @@
+// hpr_update.cuh — row-wise passes of the HPR iteration and of the KKT check.
+//
+// Each pass is one coalesced sweep that applies, per row / column, the whole
+// chain of numpy operations the reference spreads over ~15 array
+// temporaries (hprlp.py:190-203), in the reference's evaluation order.
+//
+// Twin folding.  SCUC flow rows come in (lo, hi) pairs whose coefficients are
+// exact negatives (formulation.py:366-369; preserved by diagonal scaling
+// because both rows have the same norms).  The engine stores each pair once
+// ("folded" row f covering rows frow[f] .. frow[f+1]-1, at most two):
+//   (A x)_i   = s_f  and  (A x)_{i+1} = -s_f                (exact negation)
+//   (A^T y)_j gathers y_fold[f] = y_i - y_{i+1}             (one product per pair)
+// so both iteration products read the flow block once instead of twice.
+#pragma once
+
+#include "hpr_spmv.cuh"
+
+namespace hpr {
+
+__device__ __forceinline__ double halpern_t(const Ctrl* c, int j) {
+    return 1.0 / ((double)(c->k0 + j) + 2.0);
+}
+
+// ---------------------------------------------------------------------------
+// primal half of hpr_iterate, one column j per thread (hprlp.py:190-192,
+// 196, 198, 200-203):  g = x + sigma (A^T y - c);  bar_x = clip(g, l, u);
+// bar_z = (bar_x - g) / sigma;  x~ = 2 bar_x - x;  x, z <- Halpern
+// ---------------------------------------------------------------------------
+template <typename T>
+struct PrimalArgs {
+    const Ctrl* ctrl;
+    int j_in_block;
+    int n;
+    const T* aty;               // A^T y (product vector)
+    T *X, *Z, *XT;
+    const T *AX, *AZ, *C, *LO, *UP;
+    T *BX, *BZ;                 // CHECK: bar iterates (work dtype)
+    double *XM, *ZM;            // CHECK: master-space bars (to_master, hprlp.py:272-276)
+    const double* CS;
+};
+
+template <typename T, bool CHECK>
+__global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
+    const double td = halpern_t(a.ctrl, a.j_in_block);
+    const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
+    const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
+    for (int j = blockIdx.x * TPB + threadIdx.x; j < a.n; j += gridDim.x * TPB) {
+        const T x = a.X[j], z = a.Z[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
+        const T ax = a.AX[j], az = a.AZ[j], p = a.aty[j];
+        const T g = x + sig * (p - c);
+        const T bx = np_clip(g, lo, up);
+        const T bz = (bx - g) / sig;
+        const T xt = T(2) * bx - x;
+        const T zh = T(2) * bz - z;
+        a.XT[j] = xt;
+        a.X[j] = t * ax + omt * xt;
+        a.Z[j] = t * az + omt * zh;
+        if constexpr (CHECK) {
+            a.BX[j] = bx;
+            a.BZ[j] = bz;
+            const double cs = a.CS[j];
+            a.XM[j] = ((double)bx * cs) * bsc;
+            a.ZM[j] = ((double)bz * csc) / cs;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dual half of hpr_iterate over folded rows (hprlp.py:193-194, 197, 202):
+// bar_y = Pi_D(y + (theta - A x~)/(lambda sigma));  y <- Halpern;  y_fold
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DualArgs {
+    const Ctrl* ctrl;
+    int j_in_block;
+    int nf, n_eq;
+    const int* frow;            // nf + 1
+    const T* ax;                // folded A x~
+    T* Y;
+    const T *AY, *RHS;
+    T* YF;                      // y folded (gathered by the next A^T y)
+    T *BY, *BYF;                // CHECK
+    double *YM, *YMF;           // CHECK: master bar y and its folded form
+    const double* RS;
+};
+
+template <typename T, bool CHECK>
+__global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
+    const double td = halpern_t(a.ctrl, a.j_in_block);
+    const T inv = (T)(1.0 / (a.ctrl->lam * a.ctrl->sigma)), t = (T)td, omt = (T)(1.0 - td);
+    const double csc = a.ctrl->c_scale;
+    for (int f = blockIdx.x * TPB + threadIdx.x; f < a.nf; f += gridDim.x * TPB) {
+        const int i0 = a.frow[f], cnt = a.frow[f + 1] - i0;
+        const T s = a.ax[f];
+        T yn[2], byv[2];
+        double ym[2];
+        for (int q = 0; q < cnt; ++q) {
+            const int i = i0 + q;
+            const T axi = q ? -s : s;
+            const T y = a.Y[i];
+            const T v = y + inv * (a.RHS[i] - axi);
+            const T by = i >= a.n_eq ? np_max(v, T(0)) : v;
+            const T yh = T(2) * by - y;
+            yn[q] = t * a.AY[i] + omt * yh;
+            a.Y[i] = yn[q];
+            if constexpr (CHECK) {
+                byv[q] = by;
+                a.BY[i] = by;
+                ym[q] = ((double)by * a.RS[i]) * csc;
+                a.YM[i] = ym[q];
+            }
+        }
+        a.YF[f] = cnt == 2 ? yn[0] - yn[1] : yn[0];
+        if constexpr (CHECK) {
+            a.BYF[f] = cnt == 2 ? byv[0] - byv[1] : byv[0];
+            a.YMF[f] = cnt == 2 ? ym[0] - ym[1] : ym[0];
+        }
+    }
+}
+
+// y_fold / bar_y_fold / y_m_fold from unfolded vectors (any pointer may be null)
+template <typename T>
+__global__ void k_fold_rows(int nf, const int* frow, const T* Y, T* YF, const T* BY, T* BYF,
+                            const double* YM, double* YMF) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int i0 = frow[f];
+    const bool pair = frow[f + 1] - i0 == 2;
+    if (YF) YF[f] = pair ? Y[i0] - Y[i0 + 1] : Y[i0];
+    if (BYF) BYF[f] = pair ? BY[i0] - BY[i0 + 1] : BY[i0];
+    if (YMF) YMF[f] = pair ? YM[i0] - YM[i0 + 1] : YM[i0];
+}
+
+// ---------------------------------------------------------------------------
+// KKT check terms, master data (hprlp.py:116-139 with _dual_objective :98-113),
+// plus ||bar - anchor|| for the sigma update (:437-438) and the finiteness test
+// (:406-407).  Block partial sums (fixed order) -> part[k * gridDim.x + block].
+// ---------------------------------------------------------------------------
+template <typename T>
+struct CheckRowsArgs {
+    int nf, n_eq;
+    const int* frow;
+    const double* ax;           // folded A_m x_m
+    const double *YM, *RHSM;
+    const T *BY, *AY;
+    double* part;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TPB) k_check_rows(CheckRowsArgs<T> a) {
+    Acc<KR> acc;
+    acc.zero();
+    for (int f = blockIdx.x * TPB + threadIdx.x; f < a.nf; f += gridDim.x * TPB) {
+        const int i0 = a.frow[f], cnt = a.frow[f + 1] - i0;
+        const double s = a.ax[f];
+        for (int q = 0; q < cnt; ++q) {
+            const int i = i0 + q;
+            const double axi = q ? -s : s;
+            const double ym = a.YM[i], rhs = a.RHSM[i];
+            const double v = (ym - axi) + rhs;
+            const double pr = i >= a.n_eq ? np_max(v, 0.0) : v;
+            const double pv = ym - pr;
+            acc.v[0] += pv * pv;
+            acc.v[1] += rhs * ym;
+            const T by = a.BY[i];
+            const double d = (double)(by - a.AY[i]);
+            acc.v[2] += d * d;
+            acc.v[3] += finite(by) ? 0.0 : 1.0;
+        }
+    }
+    block_store<KR>(acc, a.part, gridDim.x, blockIdx.x);
+}
+
+template <typename T>
+struct CheckColsArgs {
+    int n;
+    const double* aty;          // A_m^T y_m
+    const double *XM, *ZM, *COSTM, *LOM, *UPM;
+    const T *BX, *BZ, *AX;
+    double* part;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TPB) k_check_cols(CheckColsArgs<T> a) {
+    Acc<KC> acc;
+    acc.zero();
+    for (int j = blockIdx.x * TPB + threadIdx.x; j < a.n; j += gridDim.x * TPB) {
+        const double xm = a.XM[j], zm = a.ZM[j], c = a.COSTM[j], lo = a.LOM[j], up = a.UPM[j];
+        const double dv = (c - a.aty[j]) - zm;
+        const double bv = xm - np_clip(xm - zm, lo, up);
+        acc.v[0] += dv * dv;
+        acc.v[1] += bv * bv;
+        acc.v[2] += c * xm;
+        acc.v[3] += isfinite(lo) ? lo * np_max(zm, 0.0) : 0.0;
+        acc.v[4] += isfinite(up) ? up * np_min(zm, 0.0) : 0.0;
+        const T bx = a.BX[j];
+        const double d = (double)(bx - a.AX[j]);
+        acc.v[5] += d * d;
+        acc.v[6] += (finite(bx) ? 0.0 : 1.0) + (finite(a.BZ[j]) ? 0.0 : 1.0);
+    }
+    block_store<KC>(acc, a.part, gridDim.x, blockIdx.x);
+}
+
+}  // namespace hpr

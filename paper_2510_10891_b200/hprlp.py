@@ -207,7 +207,7 @@ class Engine:
     The device workspace is a torch uint8 tensor (PyTorch owns the memory);
     the engine's kernels run on a private CUDA stream of the handle."""
 
-    def __init__(self, lp, device: int | None = None, reorder: bool = True):
+    def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("the HPR engine needs a CUDA device (no CPU fallback)")
@@ -238,7 +238,8 @@ class Engine:
         self.device = dev
         self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=f"cuda:{dev}")
         opt = _capi.Options(dev, None, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
-                            0 if reorder else _capi.HPR_FLAG_NO_REORDER)
+                            (0 if reorder else _capi.HPR_FLAG_NO_REORDER)
+                            | (0 if fold else _capi.HPR_FLAG_NO_FOLD))
         h = _capi.C.c_void_p()
         _capi.check(self._lib.hpr_create(_capi.C.byref(self._prob), _capi.C.byref(opt),
                                          _capi.C.byref(h)))
@@ -307,6 +308,12 @@ class Engine:
         _capi.check(self._lib.hpr_resume(self._h, int(more_iterations), float(tolerance),
                                          _capi.C.byref(st)))
         return st
+
+    def layout(self) -> dict:
+        """Device layout: folded rows / nonzeros, tile counts, workspace bytes."""
+        lay = _capi.Layout()
+        _capi.check(self._lib.hpr_get_layout(self._h, _capi.C.byref(lay)))
+        return {k: getattr(lay, k) for k, _ in lay._fields_}
 
     def bench_kernel(self, which: int, reps: int = 20) -> float:
         """Average device seconds of one fused iteration kernel

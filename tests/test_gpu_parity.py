@@ -211,3 +211,30 @@ def test_locality_reorder_is_transparent(H):
     assert a[3:5] == b[3:5]
     assert a[5] == pytest.approx(b[5], rel=1e-13)
     np.testing.assert_allclose(a[0], b[0], rtol=1e-7, atol=1e-9)
+
+
+def test_twin_folding_is_transparent(H):
+    """Storing (lo, hi) flow-row pairs once must not change the solve beyond
+    FP64 reassociation noise."""
+    from paper_2510_10891_b200 import scuc
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7)
+    lpa = scuc.build_relaxation(doc, scuc.sample_monitored(doc, 300, 7))
+    lp = lpa.to_lp()
+    cfg = H.SolverConfig(tolerance=1e-5, ruiz=False, log_residuals=True)
+    res = {}
+    for fold in (False, True):
+        eng = H.Engine(lp, fold=fold)
+        lay = eng.layout()
+        assert bool(lay["folded"]) == fold
+        if fold:
+            assert lay["folded_rows"] == lpa.shape[0] - 300 and lay["folded_nnz"] < lpa.nnz
+        res[fold] = eng.solve_raw(cfg)
+        eng.close()
+    (x0, y0, z0, s0, l0), (x1, y1, z1, s1, l1) = res[False], res[True]
+    assert s0.lam == s1.lam
+    assert abs(s0.iterations - s1.iterations) <= max(32, 0.02 * s0.iterations)
+    assert abs(s1.objective - s0.objective) <= 1e-6 * abs(s0.objective)
+    # identical trajectory for the first checks (reassociation noise only)
+    a = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in l0[:20]])
+    b = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in l1[:20]])
+    np.testing.assert_allclose(a, b, rtol=1e-8, atol=1e-14)

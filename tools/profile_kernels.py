@@ -1,5 +1,10 @@
-"""Launch each fused iteration kernel once outside the loop graph so ncu can
-capture it in isolation:  ncu -k regex:EpiDual|EpiPrimal ... python tools/profile_kernels.py"""
+"""Launch each kernel of one HPR iteration outside the loop graph, inside an
+NVTX range "iter", so ncu can capture them in isolation:
+
+    ncu --nvtx --nvtx-include "iter/" --set full ... python tools/profile_kernels.py --reps 1
+
+Prints the CUDA-event time of every kernel (average over --reps launches).
+"""
 import argparse
 import os
 import sys
@@ -11,6 +16,7 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--precision", default="fp64")
 ap.add_argument("--reorder", type=int, default=1)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--which", default="0,1,2,3")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -18,15 +24,17 @@ import torch  # noqa: E402
 from paper_2510_10891_b200 import hprlp, scuc  # noqa: E402
 from paper_2510_10891_b200.lp import Precision  # noqa: E402
 
+NAMES = {0: "spmv_A", 1: "spmv_AT", 2: "update_primal", 3: "update_dual", 4: "fused_A_dual",
+         5: "fused_AT_primal"}
 doc, mon, lpa = scuc.build_config(a.config, device="cuda:0")
 eng = hprlp.Engine(lpa.to_lp(), reorder=bool(a.reorder))
 eng.solve_raw(hprlp.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(a.precision),
                                  max_iterations=0))
-t_dual = eng.bench_kernel(0, a.reps)
-t_primal = eng.bench_kernel(1, a.reps)
-t_at = eng.bench_kernel(2, a.reps)
-t_a = eng.bench_kernel(3, a.reps)
 torch.cuda.synchronize()
-print(f"{os.environ.get('HPR_LIB', 'default')} {os.environ.get('HPR_SPMV', 'pipe')} {a.config} "
-      f"{lpa.shape} nnz={lpa.nnz} dual {t_dual*1e6:.1f} us primal {t_primal*1e6:.1f} us "
-      f"| plain A {t_a*1e6:.1f} us  plain AT {t_at*1e6:.1f} us")
+out = []
+with torch.cuda.nvtx.range("iter"):
+    for w in [int(v) for v in a.which.split(",")]:
+        out.append(f"{NAMES[w]} {eng.bench_kernel(w, a.reps) * 1e6:.1f} us")
+torch.cuda.synchronize()
+print(f"{os.environ.get('HPR_LIB', 'default')} {a.config} {a.precision} {lpa.shape} "
+      f"nnz={lpa.nnz} | " + " | ".join(out))
