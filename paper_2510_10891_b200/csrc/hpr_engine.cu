@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hpr_common.cuh"
@@ -70,6 +71,17 @@ namespace {
 
 inline int nblk(long long n, int tpb = TPB) {
     return (int)std::max<long long>(1, (n + tpb - 1) / tpb);
+}
+
+// cudaLaunchKernelEx wrapper (typed arguments, error check)
+template <typename... KArgs, typename... Args>
+void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) fail(HPR_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
 }
 
 // fixed grid of the row-wise passes: deterministic partial-sum slots
@@ -463,8 +475,7 @@ double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only) {
 template <typename T, class Epi>
 void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, const Epi& epi,
                  cudaStream_t s) {
-    k_spmv<T, Epi><<<M.ntiles, TPB, 0, s>>>(M.view<T>(vals), xg, epi);
-    CKL();
+    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, M.view<T>(vals), xg, epi);
     h->launches += 1;
 }
 
@@ -644,21 +655,18 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
     const int gr = row_grid(h->nf), gc = row_grid(h->n);
     CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
-    k_check_rows<T><<<gr, TPB, 0, s>>>(ar);
-    CKL();
+    launch(k_check_rows<T>, gr, TPB, s, ar);
     launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
     CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                         h->colpart};
-    k_check_cols<T><<<gc, TPB, 0, s>>>(ac);
-    CKL();
-    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, gr, h->colpart, gc, h->log, mode);
-    CKL();
+    launch(k_check_cols<T>, gc, TPB, s, ac);
+    launch(k_controller, 1, CTRL_TPB, s, h->ctrl, (const double*)h->rowpart, gr,
+           (const double*)h->colpart, gc, h->log, mode);
     const int len = std::max(h->n, h->m);
-    k_restart_copy<T><<<row_grid(len), TPB, 0, s>>>(h->ctrl, h->n, h->m, h->nf, h->XM, h->YM,
-                                                    h->ZM, h->BXm, h->BYm, h->BZm, p.X, p.Y, p.Z,
-                                                    p.AX, p.AY, p.AZ, p.BX, p.BY, p.BZ, p.YF,
-                                                    p.BYF);
-    CKL();
+    launch(k_restart_copy<T>, row_grid(len), TPB, s, (const Ctrl*)h->ctrl, h->n, h->m, h->nf,
+           (const double*)h->XM, (const double*)h->YM, (const double*)h->ZM, h->BXm, h->BYm,
+           h->BZm, p.X, p.Y, p.Z, p.AX, p.AY, p.AZ, (const T*)p.BX, (const T*)p.BY,
+           (const T*)p.BZ, p.YF, (const T*)p.BYF);
     h->launches += 4;
 }
 
@@ -668,13 +676,11 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s);                       // A^T y
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs};
-    k_update_primal<T, CHECK><<<row_grid(h->n), TPB, 0, s>>>(pa);
-    CKL();
+    launch(k_update_primal<T, CHECK>, row_grid(h->n), TPB, s, pa);
     launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s);                         // A x~
     DualArgs<T> da{h->ctrl, j, h->nf, h->n_eq, h->frow, p.P, p.Y, p.AY, p.rhs, p.YF,
                    p.BY, p.BYF, h->YM, h->YMF, h->rs};
-    k_update_dual<T, CHECK><<<row_grid(h->nf), TPB, 0, s>>>(da);
-    CKL();
+    launch(k_update_dual<T, CHECK>, row_grid(h->nf), TPB, s, da);
     h->launches += 2;
 }
 
@@ -707,8 +713,14 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     const long long l0 = h->launches;
     CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
-    for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
-    enqueue_check<T>(h, p, 1, h->cap);
+    try {
+        for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
+        enqueue_check<T>(h, p, 1, h->cap);
+    } catch (...) {
+        cudaGraph_t dummy;
+        cudaStreamEndCapture(h->cap, &dummy);
+        throw;
+    }
     cudaGraph_t captured;
     CK(cudaStreamEndCapture(h->cap, &captured));
     h->g_per_block = h->launches - l0;
