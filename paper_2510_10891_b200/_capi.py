@@ -20,6 +20,7 @@ HPR_OPTIMAL, HPR_ITERATION_LIMIT, HPR_TIME_LIMIT, HPR_NUMERICAL_FAILURE = 0, 1, 
 HPR_FP64, HPR_FP32 = 0, 1
 HPR_FLAG_NO_REORDER = 1
 HPR_FLAG_NO_FOLD = 2
+HPR_FLAG_NO_RUNS = 4
 HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",

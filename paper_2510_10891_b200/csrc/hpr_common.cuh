@@ -17,7 +17,7 @@ constexpr int TPB = 256;          // threads per CTA for every tiled kernel
 constexpr int TILE_NNZ = 2048;    // nonzeros staged per stream tile (16 KB FP64 products)
 constexpr int TILE_ROWS = TPB;    // rows per stream tile (one epilogue row per thread)
 constexpr int ITEMS = TILE_NNZ / TPB;
-constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row (one pipeline stage)
+constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row
 constexpr int MAX_B = 64;         // largest check_every the fused loop body supports
 
 // quantities accumulated by the two master-space check kernels
@@ -83,6 +83,7 @@ struct Csr {
     int nlong;
     int* counters;           // per long row, zero between launches
     double* tile_part;       // per tile partial sums of long-row chunks (work dtype)
+    const int2* taux;        // per tile {c0, 1} if the chunk's columns are c0, c0+1, ...; else {0, 0}
 };
 
 }  // namespace hpr

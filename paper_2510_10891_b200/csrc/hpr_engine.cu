@@ -94,10 +94,11 @@ inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 struct Plan {
     std::vector<int4> tiles, longs;
+    std::vector<int2> taux;          // consecutive-column chunks (see hpr_spmv.cuh)
 };
 
 // Cut a CSR into stream tiles and long-row chunks (see hpr_spmv.cuh).
-Plan build_tiles(const int32_t* ptr, int rows) {
+Plan build_tiles(const int32_t* ptr, int rows, const int32_t* idx = nullptr) {
     Plan p;
     int r = 0;
     while (r < rows) {
@@ -110,6 +111,9 @@ Plan build_tiles(const int32_t* ptr, int rows) {
                 const int e0 = ptr[r] + c * CHUNK_NNZ;
                 const int e1 = std::min(ptr[r + 1], e0 + CHUNK_NNZ);
                 p.tiles.push_back(make_int4(r, e0, e1, li));
+                bool run = idx != nullptr;
+                for (int e = e0 + 1; e < e1 && run; ++e) run = idx[e] == idx[e - 1] + 1;
+                p.taux.push_back(run ? make_int2(idx[e0], 1) : make_int2(0, 0));
             }
             ++r;
             continue;
@@ -123,6 +127,7 @@ Plan build_tiles(const int32_t* ptr, int rows) {
             ++r;
         }
         p.tiles.push_back(make_int4(r0, -(r + 1), ptr[r0], ptr[r]));
+        p.taux.push_back(make_int2(0, 0));
     }
     return p;
 }
@@ -164,6 +169,7 @@ struct DevCsr {
     float* w32 = nullptr;
     int* src = nullptr;          // folded operands: source entry in the unfolded values
     int4 *tiles = nullptr, *longs = nullptr;
+    int2* taux = nullptr;
     int ntiles = 0, nlong = 0;
     int* counters = nullptr;
     double* tpart = nullptr;
@@ -181,6 +187,7 @@ struct DevCsr {
         c.nlong = nlong;
         c.counters = counters;
         c.tile_part = tpart;
+        c.taux = taux;
         return c;
     }
     int nslots() const { return ntiles + nlong; }
@@ -248,6 +255,7 @@ size_t carve(hpr_handle* h, char* base) {
         M.longs = cv.take<int4>(tb.longs);
         M.counters = cv.take<int>(tb.longs);
         M.tpart = cv.take<double>(tb.tiles);
+        M.taux = cv.take<int2>(tb.tiles);
     };
     csr(h->A, m, bm, false, false);
     csr(h->AT, n, bn, false, false);
@@ -923,6 +931,7 @@ void upload_csr(hpr_handle* h, DevCsr& M, const HostCsr& c, int rows, int cols, 
             CK(cudaMemcpyAsync(M.src, c.src.data(), sizeof(int) * M.nnz, cudaMemcpyHostToDevice, s));
     }
     CK(cudaMemcpyAsync(M.tiles, pl.tiles.data(), sizeof(int4) * pl.tiles.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(M.taux, pl.taux.data(), sizeof(int2) * pl.taux.size(), cudaMemcpyHostToDevice, s));
     if (!pl.longs.empty()) {
         CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
@@ -1038,8 +1047,11 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             ft.src.clear();
         }
         h->nnz_f = (long long)f.idx.size();
-        Plan pa = build_tiles(a.ptr.data(), m), pt = build_tiles(at.ptr.data(), n);
-        Plan pf = build_tiles(f.ptr.data(), h->nf), pft = build_tiles(ft.ptr.data(), n);
+        const bool runs = !(flags & HPR_FLAG_NO_RUNS);
+        Plan pa = build_tiles(a.ptr.data(), m, runs ? a.idx.data() : nullptr);
+        Plan pt = build_tiles(at.ptr.data(), n, runs ? at.idx.data() : nullptr);
+        Plan pf = build_tiles(f.ptr.data(), h->nf, runs ? f.idx.data() : nullptr);
+        Plan pft = build_tiles(ft.ptr.data(), n, runs ? ft.idx.data() : nullptr);
         check_plan(pa, m, p->nnz);
         check_plan(pt, n, p->nnz);
         check_plan(pf, m, p->nnz);

@@ -14,9 +14,10 @@
 //    the short structural rows, so those sums run in index order exactly like
 //    scipy's csr_matvec.
 //  * chunk tile {row, e0, e1, li}: one CHUNK_NNZ slice of a long row (SCUC
-//    balance and PTDF flow rows, up to ~22K nonzeros).  Each CTA reduces its
+//    balance and PTDF flow rows, ~7K-22K nonzeros).  Each CTA reduces its
 //    slice; the last CTA to finish (atomic ticket) adds the slices in chunk
-//    order — deterministic — and emits the row.
+//    order — deterministic — and emits the row.  A slice whose columns are
+//    consecutive is streamed without its index array (taux).
 //
 // Kept deliberately lean (32 registers, 8 CTAs/SM): the projection /
 // Halpern update runs as a separate coalesced row-wise pass (hpr_update.cuh).
@@ -114,20 +115,38 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg
     } else {
         // ---------------- chunk of a long row {row, e0, e1, li} ----------------
         const int row = tl.x, e0 = tl.y, e1 = tl.z, li = tl.w;
+        // aux {c0, 1}: the chunk covers the consecutive columns c0 .. c0+len-1
+        // (PTDF flow rows are dense over their period's columns), so neither
+        // the index stream nor a dependent load stands between the value
+        // stream and the gathers
+        const int2 aux = A.taux[blockIdx.x];
         constexpr int IL = CHUNK_NNZ / TPB;
-        int c[IL];
-        T v[IL];
-#pragma unroll
-        for (int q = 0; q < IL; ++q) {
-            const int e = e0 + threadIdx.x + q * TPB;
-            c[q] = e < e1 ? ld_stream(A.indices + e) : 0;
-            v[q] = e < e1 ? ld_stream(A.vals + e) : T(0);
-        }
         T s = T(0);
+        if (aux.y) {
+            const T* __restrict__ xc = xg + aux.x - e0;
+            T v[IL], g[IL];
 #pragma unroll
-        for (int q = 0; q < IL; ++q) {
-            const int e = e0 + threadIdx.x + q * TPB;
-            if (e < e1) s += v[q] * ld_ro(xg + c[q]);
+            for (int q = 0; q < IL; ++q) {
+                const int e = e0 + threadIdx.x + q * TPB;
+                v[q] = e < e1 ? ld_stream(A.vals + e) : T(0);
+                g[q] = e < e1 ? ld_ro(xc + e) : T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < IL; ++q) s += v[q] * g[q];
+        } else {
+            int c[IL];
+            T v[IL];
+#pragma unroll
+            for (int q = 0; q < IL; ++q) {
+                const int e = e0 + threadIdx.x + q * TPB;
+                c[q] = e < e1 ? ld_stream(A.indices + e) : 0;
+                v[q] = e < e1 ? ld_stream(A.vals + e) : T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < IL; ++q) {
+                const int e = e0 + threadIdx.x + q * TPB;
+                if (e < e1) s += v[q] * ld_ro(xg + c[q]);
+            }
         }
         s = warp_sum(s);
         if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = s;

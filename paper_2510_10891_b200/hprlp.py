@@ -207,7 +207,8 @@ class Engine:
     The device workspace is a torch uint8 tensor (PyTorch owns the memory);
     the engine's kernels run on a private CUDA stream of the handle."""
 
-    def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True):
+    def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True,
+                 runs: bool = True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("the HPR engine needs a CUDA device (no CPU fallback)")
@@ -239,7 +240,8 @@ class Engine:
         self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=f"cuda:{dev}")
         opt = _capi.Options(dev, None, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
                             (0 if reorder else _capi.HPR_FLAG_NO_REORDER)
-                            | (0 if fold else _capi.HPR_FLAG_NO_FOLD))
+                            | (0 if fold else _capi.HPR_FLAG_NO_FOLD)
+                            | (0 if runs else _capi.HPR_FLAG_NO_RUNS))
         h = _capi.C.c_void_p()
         _capi.check(self._lib.hpr_create(_capi.C.byref(self._prob), _capi.C.byref(opt),
                                          _capi.C.byref(h)))
