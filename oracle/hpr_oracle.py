@@ -65,6 +65,8 @@ class OracleConfig:
             return cls()
         if isinstance(cfg, cls):
             return cfg
+        if isinstance(cfg, dict):
+            return cls(**cfg)
         kw = {k: getattr(cfg, k) for k in cls.__dataclass_fields__ if hasattr(cfg, k)}
         p = kw.get("precision")
         if p is not None and not isinstance(p, str):
