@@ -85,7 +85,7 @@ void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&.
 }
 
 // fixed grid of the row-wise passes: deterministic partial-sum slots
-constexpr int ROW_GRID_MAX = 148 * 8;
+constexpr int ROW_GRID_MAX = 148 * 32;
 inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 // ===========================================================================
@@ -203,6 +203,7 @@ struct hpr_handle {
     DevCsr A, AT, F, FT;
     bool folded = false;
     int* frow = nullptr;                     // nf + 1 folded-row starts
+    int* rmap = nullptr;                     // m: 2 * folded row + second-of-pair
     // vectors (engine order)
     double *rhs_m, *cost_m, *lo_m, *up_m, *rs, *cs, *fr, *fc;
     double *rhs_w, *cost_w, *lo_w, *up_w;    // FP64 work (setup)
@@ -262,6 +263,7 @@ size_t carve(hpr_handle* h, char* base) {
     csr(h->F, m, bm, true, true);
     csr(h->FT, n, bn, true, true);
     h->frow = cv.take<int>(m + 1);
+    h->rmap = cv.take<int>(m);
     for (double** v : {&h->rhs_m, &h->rs, &h->fr, &h->rhs_w, &h->YM, &h->YMF, &h->BYm})
         *v = cv.take<double>(m);
     for (double** v : {&h->cost_m, &h->lo_m, &h->up_m, &h->cs, &h->fc, &h->cost_w, &h->lo_w,
@@ -684,11 +686,11 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s);                       // A^T y
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs};
-    launch(k_update_primal<T, CHECK>, row_grid(h->n), TPB, s, pa);
+    launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
     launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s);                         // A x~
-    DualArgs<T> da{h->ctrl, j, h->nf, h->n_eq, h->frow, p.P, p.Y, p.AY, p.rhs, p.YF,
+    DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                    p.BY, p.BYF, h->YM, h->YMF, h->rs};
-    launch(k_update_dual<T, CHECK>, row_grid(h->nf), TPB, s, da);
+    launch(k_update_dual<T, CHECK>, nblk(h->m), TPB, s, da);
     h->launches += 2;
 }
 
@@ -1083,6 +1085,13 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         upload_csr(h, h->F, f, h->nf, n, pf, h->folded);
         upload_csr(h, h->FT, ft, n, h->nf, pft, h->folded);
         CK(cudaMemcpyAsync(h->frow, frow.data(), sizeof(int) * frow.size(), cudaMemcpyHostToDevice, s));
+        {
+            std::vector<int32_t> rmap(m);
+            for (int f = 0; f < h->nf; ++f)
+                for (int i = frow[f]; i < frow[f + 1]; ++i) rmap[i] = 2 * f + (i > frow[f] ? 1 : 0);
+            CK(cudaMemcpyAsync(h->rmap, rmap.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        }
         if (h->reordered) {
             CK(cudaMemcpyAsync(h->rperm, rperm.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
             CK(cudaMemcpyAsync(h->cperm, cperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
@@ -1372,13 +1381,13 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
         EpiStore<T> st{p.P, nullptr};
         PrimalArgs<T> pa{h->ctrl, 0, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                          p.BX, p.BZ, h->XM, h->ZM, h->cs};
-        DualArgs<T> da{h->ctrl, 0, h->nf, h->n_eq, h->frow, p.P, p.Y, p.AY, p.rhs, p.YF,
+        DualArgs<T> da{h->ctrl, 0, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                        p.BY, p.BYF, h->YM, h->YMF, h->rs};
         switch (which) {
             case 0: launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s); break;
             case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s); break;
-            case 2: k_update_primal<T, false><<<row_grid(h->n), TPB, 0, s>>>(pa); break;
-            default: k_update_dual<T, false><<<row_grid(h->nf), TPB, 0, s>>>(da); break;
+            case 2: k_update_primal<T, false><<<nblk(h->n), TPB, 0, s>>>(pa); break;
+            default: k_update_dual<T, false><<<nblk(h->m), TPB, 0, s>>>(da); break;
         }
         CKL();
     };

@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
     const double td = halpern_t(a.ctrl, a.j_in_block);
     const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
     const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
-    for (int j = blockIdx.x * TPB + threadIdx.x; j < a.n; j += gridDim.x * TPB) {
+    const int j = blockIdx.x * TPB + threadIdx.x;
+    if (j < a.n) {
         const T x = a.X[j], z = a.Z[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
         const T ax = a.AX[j], az = a.AZ[j], p = a.aty[j];
         const T g = x + sig * (p - c);
@@ -66,15 +67,18 @@ __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
 }
 
 // ---------------------------------------------------------------------------
-// dual half of hpr_iterate over folded rows (hprlp.py:193-194, 197, 202):
-// bar_y = Pi_D(y + (theta - A x~)/(lambda sigma));  y <- Halpern;  y_fold
+// dual half of hpr_iterate, one row i per thread (hprlp.py:193-194, 197, 202):
+// bar_y = Pi_D(y + (theta - A x~)/(lambda sigma));  y <- Halpern.  rmap[i] =
+// 2 f + (i is the second row of twin pair f); (A x~)_i = +-P[f].  The thread
+// of a pair's first row also forms y_fold[f] = y_i - y_{i+1} (it recomputes
+// the partner's update from L1-resident operands instead of synchronising).
 // ---------------------------------------------------------------------------
 template <typename T>
 struct DualArgs {
     const Ctrl* ctrl;
     int j_in_block;
-    int nf, n_eq;
-    const int* frow;            // nf + 1
+    int m, n_eq;
+    const int* rmap;            // m: 2 * folded row + second-of-pair flag
     const T* ax;                // folded A x~
     T* Y;
     const T *AY, *RHS;
@@ -84,36 +88,52 @@ struct DualArgs {
     const double* RS;
 };
 
+template <typename T>
+struct DualRow {
+    T yn, by;
+};
+
+template <typename T>
+__device__ __forceinline__ DualRow<T> dual_row(T y, T rhs, T ay, T ax, bool ineq, T inv, T t,
+                                               T omt) {
+    const T v = y + inv * (rhs - ax);
+    const T by = ineq ? np_max(v, T(0)) : v;
+    const T yh = T(2) * by - y;
+    return {t * ay + omt * yh, by};
+}
+
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
+    const int i = blockIdx.x * TPB + threadIdx.x;
+    if (i >= a.m) return;
     const double td = halpern_t(a.ctrl, a.j_in_block);
     const T inv = (T)(1.0 / (a.ctrl->lam * a.ctrl->sigma)), t = (T)td, omt = (T)(1.0 - td);
-    const double csc = a.ctrl->c_scale;
-    for (int f = blockIdx.x * TPB + threadIdx.x; f < a.nf; f += gridDim.x * TPB) {
-        const int i0 = a.frow[f], cnt = a.frow[f + 1] - i0;
-        const T s = a.ax[f];
-        T yn[2], byv[2];
-        double ym[2];
-        for (int q = 0; q < cnt; ++q) {
-            const int i = i0 + q;
-            const T axi = q ? -s : s;
-            const T y = a.Y[i];
-            const T v = y + inv * (a.RHS[i] - axi);
-            const T by = i >= a.n_eq ? np_max(v, T(0)) : v;
-            const T yh = T(2) * by - y;
-            yn[q] = t * a.AY[i] + omt * yh;
-            a.Y[i] = yn[q];
-            if constexpr (CHECK) {
-                byv[q] = by;
-                a.BY[i] = by;
-                ym[q] = ((double)by * a.RS[i]) * csc;
-                a.YM[i] = ym[q];
+    const int code = a.rmap[i];
+    const int f = code >> 1;
+    const bool second = code & 1;
+    const T s = a.ax[f];
+    const DualRow<T> r = dual_row(a.Y[i], a.RHS[i], a.AY[i], second ? -s : s, i >= a.n_eq, inv,
+                                  t, omt);
+    const bool first_of_pair = !second && i + 1 < a.m && a.rmap[i + 1] == code + 1;
+    DualRow<T> r2{T(0), T(0)};
+    if (first_of_pair)
+        r2 = dual_row(a.Y[i + 1], a.RHS[i + 1], a.AY[i + 1], -s, i + 1 >= a.n_eq, inv, t, omt);
+    a.Y[i] = r.yn;
+    if (!second) a.YF[f] = first_of_pair ? r.yn - r2.yn : r.yn;
+    if constexpr (CHECK) {
+        const double csc = a.ctrl->c_scale;
+        a.BY[i] = r.by;
+        const double ym = ((double)r.by * a.RS[i]) * csc;
+        a.YM[i] = ym;
+        if (!second) {
+            if (first_of_pair) {
+                const double ym2 = ((double)r2.by * a.RS[i + 1]) * csc;
+                a.BYF[f] = r.by - r2.by;
+                a.YMF[f] = ym - ym2;
+            } else {
+                a.BYF[f] = r.by;
+                a.YMF[f] = ym;
             }
-        }
-        a.YF[f] = cnt == 2 ? yn[0] - yn[1] : yn[0];
-        if constexpr (CHECK) {
-            a.BYF[f] = cnt == 2 ? byv[0] - byv[1] : byv[0];
-            a.YMF[f] = cnt == 2 ? ym[0] - ym[1] : ym[0];
         }
     }
 }
