@@ -85,6 +85,14 @@ typedef struct hpr_options {
     void* workspace;           /* device memory owned by the caller (e.g. a torch tensor), or NULL */
     size_t workspace_bytes;
     int32_t flags;             /* HPR_FLAG_* */
+    /* Row-partitioned solve: the problem passed to
+     * hpr_create is this rank's row block (all n columns); the ranks of
+     * nccl_comm (an ncclComm_t from hpr_nccl_comm_init) exchange the A^T y
+     * partials, the column norms and the row-side check sums.  world_size
+     * <= 1 or nccl_comm == NULL is the single-GPU engine. */
+    void* nccl_comm;
+    int32_t world_size;
+    int32_t rank;
 } hpr_options;
 
 /* SolverConfig (hprlp.py:34-60), field for field. */
@@ -188,6 +196,14 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
                 const double* x, const double* y, const double* z, const double* ax,
                 const double* ay, const double* az, double* x_out, double* y_out,
                 double* z_out, double* bar_x, double* bar_y, double* bar_z);
+
+/* NCCL plumbing for the row-partitioned mode: rank 0 creates the id, the
+ * caller broadcasts its 128 bytes (e.g. over torch.distributed), every rank
+ * joins.  The communicator outlives the handles that use it. */
+int hpr_nccl_unique_id(uint8_t out[128]);
+int hpr_nccl_comm_init(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
+                       void** comm_out);
+void hpr_nccl_comm_destroy(void* comm);
 
 /* Device layout of an uploaded LP (engine introspection). */
 typedef struct hpr_layout {

@@ -26,7 +26,8 @@ HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
            "hpr_destroy", "hpr_solve", "hpr_get_log", "hpr_matvec", "hpr_kkt_residual",
            "hpr_power_method", "hpr_iterate", "hpr_resume", "hpr_bench_kernel",
-           "hpr_get_layout")
+           "hpr_get_layout", "hpr_nccl_unique_id", "hpr_nccl_comm_init",
+           "hpr_nccl_comm_destroy")
 
 _p = C.c_void_p
 
@@ -41,7 +42,8 @@ class Problem(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("stream", _p), ("workspace", _p),
-                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32)]
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_int32), ("nccl_comm", _p),
+                ("world_size", C.c_int32), ("rank", C.c_int32)]
 
 
 class Params(C.Structure):
@@ -123,6 +125,11 @@ def load(path: str | None = None):
     lib.hpr_resume.argtypes = [_p, C.c_int64, C.c_double, C.POINTER(Stats)]
     lib.hpr_bench_kernel.argtypes = [_p, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
     lib.hpr_get_layout.argtypes = [_p, C.POINTER(Layout)]
+    lib.hpr_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8 * 128)]
+    lib.hpr_nccl_comm_init.argtypes = [C.POINTER(C.c_uint8 * 128), C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(_p)]
+    lib.hpr_nccl_comm_destroy.argtypes = [_p]
+    lib.hpr_nccl_comm_destroy.restype = None
     _LIB = lib
     return lib
 

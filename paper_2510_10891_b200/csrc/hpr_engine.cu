@@ -24,6 +24,7 @@
 // inside a conditional WHILE graph node: the host launches one graph per
 // solve and waits once.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -232,6 +233,10 @@ struct hpr_handle {
     int last_prec = -1;
     bool reordered = false;
     int *rperm = nullptr, *cperm = nullptr;
+    // row-partitioned mode (hpr_options.nccl_comm)
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+    int* d_flag = nullptr;                   // collective stop flag (time limit)
 };
 
 namespace {
@@ -284,6 +289,7 @@ size_t carve(hpr_handle* h, char* base) {
     h->cperm = cv.take<int>(n);
     h->ctrl = cv.take<Ctrl>(1);
     h->d_dev = cv.take<unsigned long long>(2);
+    h->d_flag = cv.take<int>(1);
     return cv.off + 256;
 }
 
@@ -469,12 +475,29 @@ void validate(const hpr_problem* p) {
     if (!p->rhs || !p->cost || !p->lower || !p->upper) fail(HPR_ERR_INVALID, "LP vectors missing");
 }
 
-// deterministic ||v||^2 on the device -> host
-double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only) {
+// In-place all-reduce across the ranks of a row-partitioned solve (no-op on
+// one GPU).  NCCL collectives are stream-ordered and graph-capturable.
+void allreduce(hpr_handle* h, void* buf, size_t count, ncclDataType_t dt, ncclRedOp_t op,
+               cudaStream_t s) {
+    if (!h->comm || count == 0) return;
+    const ncclResult_t r = ncclAllReduce(buf, buf, count, dt, op, h->comm, s);
+    if (r != ncclSuccess) fail(HPR_ERR_CUDA, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+template <typename T>
+constexpr ncclDataType_t nccl_type() {
+    return sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+}
+
+// deterministic ||v||^2 on the device -> host; row vectors (global_rows) are
+// summed over the ranks of a partitioned solve, column vectors are replicated
+double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only,
+                 bool global_rows = false) {
     k_sumsq_part<<<RED_BLOCKS, TPB, 0, h->stream>>>(v, n, finite_only, h->red);
     CKL();
     k_sum_slots<<<1, TPB, 0, h->stream>>>(h->red, RED_BLOCKS, 1, h->red + RED_BLOCKS);
     CKL();
+    if (global_rows) allreduce(h, h->red + RED_BLOCKS, 1, ncclFloat64, ncclSum, h->stream);
     h->launches += 2;
     CK(cudaMemcpyAsync(h->h_scal, h->red + RED_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost,
                        h->stream));
@@ -502,7 +525,7 @@ double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, 
         if (used >= start_count) fail(HPR_ERR_POWER_NULL, "power_method exhausted start vectors");
         put_vec(h, v, start + (size_t)used * h->m, h->m, true);
         ++used;
-        const double nv = std::sqrt(dev_sumsq(h, v, h->m, 0));
+        const double nv = std::sqrt(dev_sumsq(h, v, h->m, 0, true));
         k_div<<<nblk(h->m), TPB, 0, h->stream>>>(v, h->m, nv);
         CKL();
         h->launches++;
@@ -515,9 +538,11 @@ double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, 
     EpiPower pwe{v, h->rowpart};
     for (; it < max_iter; ++it) {
         launch_spmv(h, h->AT, at_vals, (const double*)v, st, h->stream);   // u = A^T v
+        allreduce(h, u, h->n, ncclFloat64, ncclSum, h->stream);
         launch_spmv(h, h->A, a_vals, (const double*)u, pwe, h->stream);    // v = A u, sum v^2
         k_sum_slots<<<1, TPB, 0, h->stream>>>(h->rowpart, h->A.nslots(), 1, h->red);
         CKL();
+        allreduce(h, h->red, 1, ncclFloat64, ncclSum, h->stream);
         h->launches++;
         CK(cudaMemcpyAsync(h->h_scal, h->red, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -588,11 +613,13 @@ void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double
             CK(cudaMemsetAsync(h->d_dev, 0, 2 * sizeof(unsigned long long), s));
             k_row_absmax<<<nblk((long long)m * 32), TPB, 0, s>>>(h->A.ptr, h->A.w64, m, h->fr);
             k_row_absmax<<<nblk((long long)n * 32), TPB, 0, s>>>(h->AT.ptr, h->AT.w64, n, h->fc);
+            allreduce(h, h->fc, n, ncclFloat64, ncclMax, s);     // column maxima over all rows
             k_scale_factor<<<nblk(m), TPB, 0, s>>>(h->fr, h->fr, h->rs, m, h->d_dev);
             k_scale_factor<<<nblk(n), TPB, 0, s>>>(h->fc, h->fc, h->cs, n, h->d_dev + 1);
             CKL();
             h->launches += 4;
             apply();
+            allreduce(h, h->d_dev, 2, ncclUint64, ncclMax, s);   // non-negative doubles as bits
             CK(cudaMemcpyAsync(h->h_scal, h->d_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             if (std::max(h->h_scal[0], h->h_scal[1]) < 1e-6) break;
@@ -601,6 +628,7 @@ void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double
     if (prm->pock_chambolle) {
         k_row_abssum<<<nblk(m), TPB, 0, s>>>(h->A.ptr, h->A.w64, m, h->fr);
         k_row_abssum<<<nblk(n), TPB, 0, s>>>(h->AT.ptr, h->AT.w64, n, h->fc);
+        allreduce(h, h->fc, n, ncclFloat64, ncclSum, s);         // column 1-norms over all rows
         k_scale_factor<<<nblk(m), TPB, 0, s>>>(h->fr, h->fr, h->rs, m, nullptr);
         k_scale_factor<<<nblk(n), TPB, 0, s>>>(h->fc, h->fc, h->cs, n, nullptr);
         CKL();
@@ -614,7 +642,7 @@ void scale_problem(hpr_handle* h, const hpr_params* prm, double* bsc_out, double
     h->launches += 2;
     double bsc = 1.0, csc = 1.0;
     if (prm->normalize_rhs_objective) {
-        bsc = 1.0 + std::sqrt(dev_sumsq(h, h->rhs_w, m, 1));
+        bsc = 1.0 + std::sqrt(dev_sumsq(h, h->rhs_w, m, 1, true));
         csc = 1.0 + std::sqrt(dev_sumsq(h, h->cost_w, n, 0));
     }
     k_div<<<nblk(m), TPB, 0, s>>>(h->rhs_w, m, bsc);
@@ -663,10 +691,13 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     double* pd = (double*)h->P;
     EpiStore<double> st{pd, nullptr};
     launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
-    const int gr = row_grid(h->nf), gc = row_grid(h->n);
+    // partitioned: every rank uses the same slot count so the row-side sums reduce slot-wise
+    const int gr = h->comm ? ROW_GRID_MAX : row_grid(h->nf), gc = row_grid(h->n);
     CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     launch(k_check_rows<T>, gr, TPB, s, ar);
+    allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
     launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
     CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                         h->colpart};
     launch(k_check_cols<T>, gc, TPB, s, ac);
@@ -684,6 +715,7 @@ template <typename T, bool CHECK>
 void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
     EpiStore<T> st{p.P, nullptr};
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s);                       // A^T y
+    allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs};
     launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
@@ -708,18 +740,23 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     if (h->graph) cudaGraphDestroy(h->graph);
     h->gexec = nullptr;
     h->graph = nullptr;
-    // WHILE(cond) { B iterations; master check; controller; copies }
+    // single GPU: WHILE(cond) { B iterations; master check; controller; copies }
+    // partitioned: the same block body as a plain graph, relaunched by the
+    // host after a collective stop test (the NCCL calls live in the body)
     CK(cudaGraphCreate(&h->graph, 0));
-    cudaGraphConditionalHandle cond;
-    CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = cond;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, h->graph, nullptr, 0, &np));
-    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaGraph_t body = h->graph;
+    cudaGraphConditionalHandle cond = 0;
+    if (!h->comm) {
+        CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, h->graph, nullptr, 0, &np));
+        body = np.conditional.phGraph_out[0];
+    }
     const long long l0 = h->launches;
     CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
@@ -743,7 +780,43 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
 
 // Launch the cached loop graph from the current device state; returns the
 // device time of the loop (CUDA events on the handle's stream).
-double run_loop(hpr_handle* h) {
+// Partitioned mode: one block per launch; every rank reads the (identical)
+// controller status, and the wall-clock limit is agreed by a MAX all-reduce so
+// no rank leaves the collective sequence alone.
+double run_loop_partitioned(hpr_handle* h, double time_left) {
+    cudaStream_t s = h->stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    const long long t_before = h->h_ctrl->total;
+    CK(cudaEventRecord(h->ev[2], s));
+    while (true) {
+        CK(cudaGraphLaunch(h->gexec, s));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const int over = (time_left >= 0 && el > time_left) ? 1 : 0;
+        CK(cudaMemcpyAsync(h->d_flag, &over, sizeof(int), cudaMemcpyHostToDevice, s));
+        allreduce(h, h->d_flag, 1, ncclInt32, ncclMax, s);
+        int flag = 0;
+        CK(cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&h->h_scal[0], h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(&flag, &h->h_scal[0], sizeof(int));
+        if (h->h_ctrl->status != -1) break;
+        if (flag) {
+            h->h_ctrl->status = HPR_TIME_LIMIT;
+            CK(cudaMemcpyAsync(&h->ctrl->status, &h->h_ctrl->status, sizeof(int),
+                               cudaMemcpyHostToDevice, s));
+            break;
+        }
+    }
+    CK(cudaEventRecord(h->ev[3], s));
+    CK(cudaStreamSynchronize(s));
+    h->launches += h->g_per_block * ((h->h_ctrl->total - t_before) / h->g_B);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+    return ms * 1e-3;
+}
+
+double run_loop(hpr_handle* h, double time_left = -1.0) {
+    if (h->comm) return run_loop_partitioned(h, time_left);
     cudaStream_t s = h->stream;
     unsigned long long cv = h->gcond;
     CK(cudaMemcpyAsync(&h->ctrl->cond, &cv, sizeof(cv), cudaMemcpyHostToDevice, s));
@@ -792,13 +865,13 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     const double lam = power_method(h, h->A.w64, h->AT.w64, prm->power_tol, prm->power_max_iter,
                                     prm->power_inflation, prm->power_start,
                                     prm->power_start_count, &pits, &pconv);
-    const double rn = std::sqrt(dev_sumsq(h, h->rhs_w, m, 0));
+    const double rn = std::sqrt(dev_sumsq(h, h->rhs_w, m, 0, true));
     const double cn = std::sqrt(dev_sumsq(h, h->cost_w, n, 0));
     double sigma;
     if (prm->has_sigma0) sigma = prm->sigma0;
     else if (rn > 1e-12 && cn > 1e-12) sigma = rn / cn;
     else sigma = 1.0;
-    const double rhs_norm_m = std::sqrt(dev_sumsq(h, h->rhs_m, m, 0));
+    const double rhs_norm_m = std::sqrt(dev_sumsq(h, h->rhs_m, m, 0, true));
     const double cost_norm_m = std::sqrt(dev_sumsq(h, h->cost_m, n, 0));
     refresh_folded_values(h, fp32);
     if (fp32) cast_work_vectors(h);
@@ -872,16 +945,20 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     }
     st->loop_seconds = 0.0;
     if (status == -1) {
+        double time_left = -1.0;
         if (prm->time_limit >= 0) {
             const double rem = std::max(0.0, prm->time_limit - elapsed);
-            k_set_deadline<<<1, 1, 0, s>>>(h->ctrl, (unsigned long long)(rem * 1e9));
-            CKL();
-            h->launches++;
-            int one = 1;
-            CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+            time_left = rem;
+            if (!h->comm) {   // partitioned: agreed on the host per block
+                k_set_deadline<<<1, 1, 0, s>>>(h->ctrl, (unsigned long long)(rem * 1e9));
+                CKL();
+                h->launches++;
+                int one = 1;
+                CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+            }
         }
         ensure_graph<T>(h, p, B);
-        st->loop_seconds = run_loop(h);
+        st->loop_seconds = run_loop(h, time_left);
         status = h->h_ctrl->status;
         iterations = h->h_ctrl->total;
         if (status == HPR_ITERATION_LIMIT) iterations = prm->max_iterations;
@@ -993,6 +1070,11 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         if (!out) fail(HPR_ERR_INVALID, "out is NULL");
         h = new hpr_handle();
         h->dev = opt ? opt->device : 0;
+        if (opt && opt->nccl_comm) {            // partitioned mode (also with one rank)
+            h->comm = (ncclComm_t)opt->nccl_comm;
+            h->world = std::max(1, opt->world_size);
+            h->rank = opt->rank;
+        }
         CK(cudaSetDevice(h->dev));
         h->m = p->m;
         h->n = p->n;
@@ -1177,6 +1259,7 @@ int hpr_matvec(hpr_handle* h, int32_t transpose, const double* in, double* out) 
     put_vec(h, xin, in, nin, transpose != 0);
     EpiStore<double> st{h->pw, nullptr};       // pw holds m + n doubles
     launch_spmv(h, M, (const double*)M.mval, (const double*)xin, st, h->stream);
+    if (transpose) allreduce(h, h->pw, nout, ncclFloat64, ncclSum, h->stream);
     get_vec(h, out, h->pw, nout, transpose == 0);
     CK(cudaStreamSynchronize(h->stream));
     API_END
@@ -1197,7 +1280,7 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     k_fold_rows<double><<<nblk(h->nf), TPB, 0, s>>>(h->nf, h->frow, nullptr, nullptr, nullptr,
                                                      nullptr, h->YM, h->YMF);
     CKL();
-    const double rn = std::sqrt(dev_sumsq(h, h->rhs_m, h->m, 0));
+    const double rn = std::sqrt(dev_sumsq(h, h->rhs_m, h->m, 0, true));
     const double cn = std::sqrt(dev_sumsq(h, h->cost_m, h->n, 0));
     Ctrl c{};
     c.denom = (1.0 + rn) + cn;
@@ -1209,10 +1292,12 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     double* pd = (double*)h->P;
     EpiStore<double> st{pd, nullptr};
     launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
-    const int gr = row_grid(h->nf), gc = row_grid(h->n);
+    const int gr = h->comm ? ROW_GRID_MAX : row_grid(h->nf), gc = row_grid(h->n);
     CheckRowsArgs<double> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     k_check_rows<double><<<gr, TPB, 0, s>>>(ar);
+    allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
     launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
     CheckColsArgs<double> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                              h->colpart};
     k_check_cols<double><<<gc, TPB, 0, s>>>(ac);
@@ -1315,6 +1400,36 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     get(h->BZ, bar_z, n, h->ZM, false);
     CK(cudaStreamSynchronize(s));
     API_END
+}
+
+int hpr_nccl_unique_id(uint8_t out[128]) {
+    API_BEGIN
+    if (!out) fail(HPR_ERR_INVALID, "NULL argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) fail(HPR_ERR_CUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof(id));
+    API_END
+}
+
+int hpr_nccl_comm_init(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
+                       void** comm_out) {
+    API_BEGIN
+    if (!id || !comm_out || world_size < 1 || rank < 0 || rank >= world_size)
+        fail(HPR_ERR_INVALID, "bad argument");
+    CK(cudaSetDevice(device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm;
+    const ncclResult_t r = ncclCommInitRank(&comm, world_size, uid, rank);
+    if (r != ncclSuccess) fail(HPR_ERR_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    *comm_out = (void*)comm;
+    API_END
+}
+
+void hpr_nccl_comm_destroy(void* comm) {
+    if (comm) ncclCommDestroy((ncclComm_t)comm);
 }
 
 int hpr_get_layout(hpr_handle* h, hpr_layout* out) {

@@ -208,7 +208,7 @@ class Engine:
     the engine's kernels run on a private CUDA stream of the handle."""
 
     def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True,
-                 runs: bool = True):
+                 runs: bool = True, comm=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("the HPR engine needs a CUDA device (no CPU fallback)")
@@ -238,10 +238,13 @@ class Engine:
         dev = torch.cuda.current_device() if device is None else int(device)
         self.device = dev
         self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=f"cuda:{dev}")
+        flags = ((0 if reorder else _capi.HPR_FLAG_NO_REORDER)
+                 | (0 if fold else _capi.HPR_FLAG_NO_FOLD)
+                 | (0 if runs else _capi.HPR_FLAG_NO_RUNS))
+        ncomm, world, rank = (None, 1, 0) if comm is None else (comm.handle, comm.world_size,
+                                                                 comm.rank)
         opt = _capi.Options(dev, None, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
-                            (0 if reorder else _capi.HPR_FLAG_NO_REORDER)
-                            | (0 if fold else _capi.HPR_FLAG_NO_FOLD)
-                            | (0 if runs else _capi.HPR_FLAG_NO_RUNS))
+                            flags, ncomm, world, rank)
         h = _capi.C.c_void_p()
         _capi.check(self._lib.hpr_create(_capi.C.byref(self._prob), _capi.C.byref(opt),
                                          _capi.C.byref(h)))
@@ -325,12 +328,19 @@ class Engine:
                                                _capi.C.byref(sec)))
         return sec.value
 
-    def solve_raw(self, config, start=None, time_elapsed=0.0):
-        """One ``_solve_once`` on the device; returns (x, y, z, Stats, log)."""
+    def solve_raw(self, config, start=None, time_elapsed=0.0, rows=None, m_total=None):
+        """One ``_solve_once`` on the device; returns (x, y, z, Stats, log).
+        For a row block of a partitioned solve, `rows` / `m_total` select the
+        block's slice of the global power-method start vector."""
         cfg = config
         prec = _precision_value(cfg.precision)
         rng = np.random.default_rng(cfg.seed)
-        starts = [rng.standard_normal(self.m)]
+
+        def draw():
+            v = rng.standard_normal(self.m if rows is None else m_total)
+            return v if rows is None else v[rows]
+
+        starts = [draw()]
         x = np.empty(self.n)
         y = np.empty(self.m)
         z = np.empty(self.n)
@@ -360,7 +370,7 @@ class Engine:
                                        _capi.ptr(z0), _capi.ptr(x), _capi.ptr(y), _capi.ptr(z),
                                        _capi.C.byref(st))
             if code == _capi.HPR_ERR_POWER_NULL:
-                starts.append(rng.standard_normal(self.m))
+                starts.append(draw())
                 continue
             if code == _capi.HPR_ERR_EMPTY:
                 raise ValueError("power_method requires a nonzero matrix")
@@ -507,6 +517,91 @@ def write_iteration_log(path, result, solve_id: str = "solve") -> None:
         for rec in result.residual_log:
             w.writerow([solve_id, rec["iteration"], rec["epoch"], rec["rel_primal"],
                         rec["rel_dual"], rec["rel_box"], rec["rel_gap"], rec["sigma"]])
+
+
+# ---------------------------------------------------------------------------
+# row-partitioned solve across the GPUs of one node
+# ---------------------------------------------------------------------------
+
+class NcclComm:
+    """An NCCL communicator for the engine, bootstrapped over an initialised
+    torch.distributed process group (rank 0's unique id is broadcast)."""
+
+    def __init__(self, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+        self.world_size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        lib = _capi.load()
+        uid = (_capi.C.c_uint8 * 128)()
+        if self.rank == 0:
+            _capi.check(lib.hpr_nccl_unique_id(_capi.C.byref(uid)))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (_capi.C.c_uint8 * 128).from_buffer_copy(box[0])
+        dev = torch.cuda.current_device() if device is None else int(device)
+        h = _capi.C.c_void_p()
+        _capi.check(lib.hpr_nccl_comm_init(_capi.C.byref(uid), self.world_size, self.rank, dev,
+                                           _capi.C.byref(h)))
+        self.handle = h
+        self._lib = lib
+
+    def close(self):
+        if self.handle:
+            self._lib.hpr_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+def solve_partitioned(lp, config=None, start=None, comm: NcclComm | None = None, group=None):
+    """``solve`` with A row-partitioned over the ranks of `group` (one GPU per
+    rank).  Every rank passes the same full LP; each keeps its row block
+    (paper_2510_10891_b200.partition).  x, z come back replicated and y is
+    gathered, so every rank returns the full SolveResult."""
+    import torch.distributed as dist
+    from . import partition
+    config = config or SolverConfig()
+    t_start = time.perf_counter()
+    own = comm is None
+    comm = comm or NcclComm(group)
+    try:
+        csr = lp.matrix.csr
+        blocks = partition.partition_rows(csr.indptr, csr.indices, csr.data, int(lp.n_eq),
+                                          csr.shape[1], comm.world_size)
+        blk = blocks[comm.rank]
+        blp = partition.block_lp(lp, blk)
+        eng = Engine(blp, comm=comm)
+        sub_start = None
+        if start is not None:
+            sub_start = (start[0], np.asarray(start[1])[blk.rows], start[2])
+        x, yb, z, st, recs = eng.solve_raw(config, sub_start, time.perf_counter() - t_start,
+                                           rows=blk.rows, m_total=csr.shape[0])
+        parts = [None] * comm.world_size
+        dist.all_gather_object(parts, (blk.rows, yb), group=group)
+        y = np.empty(csr.shape[0])
+        for rows, yy in parts:
+            y[rows] = yy
+        eng.close()
+    finally:
+        if own:
+            comm.close()
+    status = getattr(_CLS.status, _STATUS_BY_CODE[st.status])
+    residual_log = [{"iteration": r.iteration, "epoch": r.epoch, "rel_primal": r.rel_primal,
+                     "rel_dual": r.rel_dual, "rel_box": r.rel_box, "rel_gap": r.rel_gap,
+                     "sigma": r.sigma} for r in recs] if config.log_residuals else []
+    objective = float(np.dot(_f64(lp.cost), x)) + float(getattr(lp, "offset", 0.0))
+    res = _CLS.result(x=x, y=y, z=z, status=status, objective=objective, kkt=_kkt_obj(st.kkt),
+                      iterations=int(st.iterations), restarts=int(st.restarts),
+                      solve_time=time.perf_counter() - t_start, sigma_final=st.sigma_final,
+                      lam=st.lam, residual_log=residual_log,
+                      precision_used=_precision_member(_precision_value(config.precision)))
+    try:
+        res.device_stats = {"loop_seconds": st.loop_seconds, "gpu_launches": int(st.gpu_launches),
+                            "world_size": comm.world_size, "block_rows": int(blk.rows.size),
+                            "block_nnz": int(blk.nnz)}
+    except AttributeError:
+        pass
+    return res
 
 
 # ---------------------------------------------------------------------------

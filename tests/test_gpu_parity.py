@@ -296,3 +296,37 @@ def test_c1_against_reference_trajectory(H):
             np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
         else:
             assert abs(r.objective - gg["objective"]) <= 1e-4 * abs(gg["objective"])
+
+
+def test_partitioned_engine_single_rank(H):
+    """The row-partitioned engine mode (NCCL all-reduces captured in the block
+    graph, host-driven block loop, collective stop test) run with one rank
+    must reproduce the single-GPU solve; the multi-rank algebra itself is
+    covered on CPU by tests/test_partitioned.py (gloo, 2 ranks)."""
+    import os
+    import torch.distributed as dist
+    from paper_2510_10891_b200 import scuc
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29613")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        doc = scuc.generate_instance(60, 20, 90, 12, seed=7)
+        lpa = scuc.build_relaxation(doc, scuc.sample_monitored(doc, 200, 7))
+        lp = lpa.to_lp()
+        cfg = H.SolverConfig(tolerance=1e-5, ruiz=True, log_residuals=True)
+        ref = H.solve(lp, cfg)
+        comm = H.NcclComm()
+        try:
+            r = H.solve_partitioned(lp, cfg, comm=comm)
+            r_tl = H.solve_partitioned(lp, H.SolverConfig(tolerance=1e-12, time_limit=0.3,
+                                                          max_iterations=10**8), comm=comm)
+        finally:
+            comm.close()
+    finally:
+        dist.destroy_process_group()
+    assert r.status.value == ref.status.value == "optimal-tolerance"
+    assert r.lam == pytest.approx(ref.lam, rel=1e-12)
+    assert abs(r.iterations - ref.iterations) <= max(32, 0.02 * ref.iterations)
+    assert abs(r.objective - ref.objective) <= 1e-7 * abs(ref.objective)
+    assert O.kkt(O.Problem.from_lp(lpa), r.x, r.y, r.z).max_rel <= 1e-5 * 1.000001
+    assert r_tl.status.value == "time-limit"
