@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"],
+                    help="N>1: independent replicas (weak scaling) or one LP row-partitioned "
+                         "over the N GPUs with NCCL (strong scaling)")
     return ap.parse_args()
 
 
@@ -190,11 +193,26 @@ def run_b200(args):
     nnz = lpa.nnz
     s = 8 if args.precision == "fp64" else 4
     lp = lpa.to_lp()
-    eng = hprlp.Engine(lp, device=local)
-    lay = eng.layout()
+    partitioned = args.mode == "partitioned"
     cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(args.precision),
                              max_iterations=max(1, args.warmup) * BLOCK)
-    x, y, z, st0, _ = eng.solve_raw(cfg)                  # setup + W warm-up blocks
+    comm = blk = None
+    if partitioned:
+        from paper_2510_10891_b200 import partition
+        if ws == 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        comm = hprlp.NcclComm()
+        blk = partition.partition_rows(lpa.indptr, lpa.indices, lpa.data, lpa.n_eq, n,
+                                       comm.world_size)[comm.rank]
+        eng = hprlp.Engine(partition.block_lp(lp, blk), device=local, comm=comm)
+        x, y, z, st0, _ = eng.solve_raw(cfg, rows=blk.rows, m_total=m)
+    else:
+        eng = hprlp.Engine(lp, device=local)
+        x, y, z, st0, _ = eng.solve_raw(cfg)              # setup + W warm-up blocks
+    lay = eng.layout()
     # timed region: exactly K blocks of the device-resident loop
     if ws > 1:
         torch.distributed.barrier()
@@ -212,7 +230,7 @@ def run_b200(args):
         tt = torch.tensor([t_loop], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_loop = float(tt.item())
-    value = ws * its / t_loop
+    value = (1 if partitioned else ws) * its / t_loop
 
     bm = bytes_model(m, n, nnz, s)
     nf, nnzf = lay["folded_rows"], lay["folded_nnz"]
@@ -230,7 +248,8 @@ def run_b200(args):
     out = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_loop / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if partitioned else "weak",
+        "vs_baseline": None,
         "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: synthetic 13659-bus/4092-unit/36-period SCUC "
                                f"LP relaxation + {args.triples or 1000} base flow triples",
@@ -240,7 +259,8 @@ def run_b200(args):
                                      "reordered": bool(lay["reordered"]),
                                      "twin_folded": bool(lay["folded"])},
                    "l2": "inputs larger than L2 (matrix stream > 1 GB/iteration)",
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single"},
+                   "parallelism": (f"rowpart{ws}" if partitioned else
+                                   (f"replicas{ws}" if ws > 1 else "single"))},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                      "bytes_per_launch": dom_b, "seconds_per_launch": dom_t,
@@ -260,7 +280,9 @@ def run_b200(args):
     }
     out["clocks"] = clk.summary()
 
-    if not args.no_e2e:
+    if partitioned:
+        out["config"]["block"] = {"rows": int(blk.rows.size), "nnz": int(blk.nnz)}
+    if not args.no_e2e and not partitioned:
         # public API from host buffers: upload + setup + solve to 1e-4 + copy back
         lp_host = lpa.to_lp()
         torch.cuda.synchronize()
@@ -285,7 +307,10 @@ def run_b200(args):
                                          f"{os.cpu_count()} host cores available)"}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if ws > 1:
+    if comm is not None:
+        eng.close()
+        comm.close()
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
