@@ -13,8 +13,8 @@
 
 namespace hpr {
 
-constexpr int TPB = 256;          // threads per CTA for every tiled kernel
-constexpr int TILE_NNZ = 2048;    // nonzeros staged per stream tile (16 KB FP64 products)
+constexpr int TPB = 128;          // threads per CTA for every tiled kernel
+constexpr int TILE_NNZ = 1024;    // nonzeros staged per stream tile (8 KB FP64 products; 8 per thread)
 constexpr int TILE_ROWS = TPB;    // rows per stream tile (one epilogue row per thread)
 constexpr int ITEMS = TILE_NNZ / TPB;
 constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row
