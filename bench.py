@@ -222,6 +222,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         ktimes = {name: eng.bench_kernel(which, args.kernel_reps) for name, which in
                   (("spmv_A", 0), ("spmv_AT", 1), ("update_primal", 2), ("update_dual", 3))}
+        t_check = eng.bench_kernel(4, 4)     # one KKT check block (mutates state: last)
     if ws > 1:
         torch.distributed.barrier()
     t_loop = st.loop_seconds
@@ -275,6 +276,9 @@ def run_b200(args):
                     for k, t in ktimes.items()},
         "iteration_us": 1e6 * t_loop / its,
         "kernel_sum_us": 1e6 * sum(ktimes.values()),
+        "check_block_us": 1e6 * t_check,
+        "launch_gap_us_per_iteration": 1e6 * (t_loop / its - sum(ktimes.values())
+                                              - t_check / BLOCK),
         "gpu_launches": int(st.gpu_launches),
         "setup": {"build_lp_s": t_build, "warmup_setup_s": st0.setup_seconds},
     }

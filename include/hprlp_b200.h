@@ -222,7 +222,8 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out);
  * hpr_bench_kernel: average device time of one kernel of the iteration,
  * launched reps times outside the graph on the handle's stream:
  * which = 0: A x~ product; 1: A^T y product; 2: primal row-wise update
- * (projection + reflection + Halpern); 3: dual row-wise update. */
+ * (projection + reflection + Halpern); 3: dual row-wise update; 4: one KKT
+ * check block (mutates the solver state: call after the measurements). */
 int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* stats);
 int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds_per_launch);
 

@@ -1486,10 +1486,12 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     API_BEGIN
     if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
-    if (which < 0 || which > 3) fail(HPR_ERR_INVALID, "unknown kernel");
+    if (which < 0 || which > 4) fail(HPR_ERR_INVALID, "unknown kernel");
     CK(cudaSetDevice(h->dev));
     cudaStream_t s = h->stream;
-    // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update
+    // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update,
+    //        4 = one whole KKT check (2 master products, row/col terms, controller, copies;
+    //            mutates the solver state — call last)
     auto body = [&](auto tag) {
         using T = decltype(tag);
         Ptrs<T> p = ptrs<T>(h);
@@ -1502,7 +1504,8 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
             case 0: launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s); break;
             case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s); break;
             case 2: k_update_primal<T, false><<<nblk(h->n), TPB, 0, s>>>(pa); break;
-            default: k_update_dual<T, false><<<nblk(h->m), TPB, 0, s>>>(da); break;
+            case 3: k_update_dual<T, false><<<nblk(h->m), TPB, 0, s>>>(da); break;
+            default: enqueue_check<T>(h, p, 1, s); break;
         }
         CKL();
     };
