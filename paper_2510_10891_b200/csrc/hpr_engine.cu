@@ -40,6 +40,7 @@
 #include "hpr_setup.cuh"
 #include "hpr_spmv.cuh"
 #include "hpr_update.cuh"
+#include "hpr_layout.cuh"
 #include "../../include/hprlp_b200.h"
 
 using namespace hpr;
@@ -95,11 +96,10 @@ inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 struct Plan {
     std::vector<int4> tiles, longs;
-    std::vector<int2> taux;          // consecutive-column chunks (see hpr_spmv.cuh)
 };
 
 // Cut a CSR into stream tiles and long-row chunks (see hpr_spmv.cuh).
-Plan build_tiles(const int32_t* ptr, int rows, const int32_t* idx = nullptr) {
+Plan build_tiles(const int32_t* ptr, int rows) {
     Plan p;
     int r = 0;
     while (r < rows) {
@@ -112,9 +112,6 @@ Plan build_tiles(const int32_t* ptr, int rows, const int32_t* idx = nullptr) {
                 const int e0 = ptr[r] + c * CHUNK_NNZ;
                 const int e1 = std::min(ptr[r + 1], e0 + CHUNK_NNZ);
                 p.tiles.push_back(make_int4(r, e0, e1, li));
-                bool run = idx != nullptr;
-                for (int e = e0 + 1; e < e1 && run; ++e) run = idx[e] == idx[e - 1] + 1;
-                p.taux.push_back(run ? make_int2(idx[e0], 1) : make_int2(0, 0));
             }
             ++r;
             continue;
@@ -128,7 +125,6 @@ Plan build_tiles(const int32_t* ptr, int rows, const int32_t* idx = nullptr) {
             ++r;
         }
         p.tiles.push_back(make_int4(r0, -(r + 1), ptr[r0], ptr[r]));
-        p.taux.push_back(make_int2(0, 0));
     }
     return p;
 }
@@ -294,138 +290,99 @@ size_t carve(hpr_handle* h, char* base) {
 }
 
 // ===========================================================================
-// host-side layout: transpose, locality ordering, twin folding
+// device-side layout build (hpr_layout.cuh): transpose, locality ordering
+// (SURVEY.md §7 hard part 5), twin folding
 // ===========================================================================
 
-struct HostCsr {
-    std::vector<int32_t> ptr, idx;
-    std::vector<double> val;
-    std::vector<int32_t> src;    // only for folded operands
-};
-
-void host_transpose(int m, int n, const HostCsr& a, HostCsr& t) {
-    const long long nnz = a.ptr[m];
-    t.ptr.assign(n + 1, 0);
-    for (long long e = 0; e < nnz; ++e) t.ptr[a.idx[e] + 1]++;
-    for (int j = 0; j < n; ++j) t.ptr[j + 1] += t.ptr[j];
-    std::vector<int32_t> next(t.ptr.begin(), t.ptr.end() - 1);
-    t.idx.resize(nnz);
-    t.val.resize(nnz);
-    for (int i = 0; i < m; ++i)
-        for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e) {
-            const int p = next[a.idx[e]]++;
-            t.idx[p] = i;
-            t.val[p] = a.val[e];
-        }
-}
-
-// Locality ordering (SURVEY.md §7 hard part 5).  The reference lays
-// variables out [g, t] (formulation.py:53-69), so a period-t flow row
-// gathers x at stride T.  Columns are regrouped by the first long row
-// (> LONG_ROW nonzeros) that touches them — for SCUC the balance row of
-// their period — and rows (equalities and inequalities separately, so the
-// n_eq prefix is preserved) by their smallest new column.  Entry order
-// inside every row of A and A^T stays the original one, so every row sum
-// keeps the reference's summation order; only the labels move.
+// Locality ordering.  The reference lays variables out [g, t]
+// (formulation.py:53-69), so a period-t flow row gathers x at stride T.
+// Columns are regrouped by the first long row (> LONG_ROW nonzeros) that
+// touches them — for SCUC the balance row of their period — and rows
+// (equalities and inequalities separately, so the n_eq prefix is preserved)
+// by their smallest new column.  Entry order inside every row of A and A^T
+// stays the original one, so every row sum keeps the reference's summation
+// order; only the labels move.
 constexpr int LONG_ROW = 256;
 
-void compute_order(int m, int n, int n_eq, const HostCsr& a, std::vector<int32_t>& rperm,
-                   std::vector<int32_t>& cperm) {
-    const int INF = 0x7fffffff;
-    std::vector<int32_t> ckey(n, INF);
-    for (int i = 0; i < m; ++i)
-        if (a.ptr[i + 1] - a.ptr[i] > LONG_ROW)
-            for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e)
-                if (ckey[a.idx[e]] == INF) ckey[a.idx[e]] = i;
-    cperm.resize(n);
-    for (int j = 0; j < n; ++j) cperm[j] = j;
-    std::stable_sort(cperm.begin(), cperm.end(), [&](int x, int y) { return ckey[x] < ckey[y]; });
-    std::vector<int32_t> cinv(n);
-    for (int k = 0; k < n; ++k) cinv[cperm[k]] = k;
-    std::vector<int32_t> rkey(m, INF);
-    for (int i = 0; i < m; ++i)
-        for (int e = a.ptr[i]; e < a.ptr[i + 1]; ++e) rkey[i] = std::min(rkey[i], cinv[a.idx[e]]);
-    rperm.resize(m);
-    for (int i = 0; i < m; ++i) rperm[i] = i;
-    auto by = [&](int x, int y) { return rkey[x] < rkey[y]; };
-    std::stable_sort(rperm.begin(), rperm.begin() + n_eq, by);
-    std::stable_sort(rperm.begin() + n_eq, rperm.end(), by);
+// scratch owned by one hpr_create call (stream-ordered pool allocations)
+struct Scratch {
+    cudaStream_t s = nullptr;
+    std::vector<void*> blocks;
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, sizeof(T) * std::max<size_t>(count, 1), s));
+        blocks.push_back(p);
+        return (T*)p;
+    }
+    ~Scratch() {
+        if (s) cudaStreamSynchronize(s);
+        for (void* p : blocks) cudaFreeAsync(p, s);
+        if (s) cudaStreamSynchronize(s);
+    }
+};
+
+// Host -> device upload of a pageable array through two pinned bounce
+// buffers (host memcpy of chunk k+1 overlaps the DMA of chunk k); several
+// times faster than a pageable cudaMemcpy for the 0.5 GB CSR of C4.
+void upload_pageable(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t CH = 32u << 20;
+    if (bytes < 2 * CH) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    char* buf = nullptr;
+    CK(cudaMallocHost(&buf, 2 * CH));
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    for (size_t off = 0, k = 0; off < bytes; off += CH, k ^= 1) {
+        const size_t len = std::min(CH, bytes - off);
+        if (used[k]) CK(cudaEventSynchronize(ev[k]));
+        std::memcpy(buf + k * CH, (const char*)src + off, len);
+        CK(cudaMemcpyAsync((char*)dst + off, buf + k * CH, len, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ev[k], s));
+        used[k] = true;
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(buf);
 }
 
-// relabel: new row r' = old row perm_rows[r'], columns through inv_cols
-void permute_csr(int rows, const HostCsr& a, const std::vector<int32_t>& perm_rows,
-                 const std::vector<int32_t>& inv_cols, HostCsr& out) {
-    out.ptr.assign(rows + 1, 0);
-    for (int r = 0; r < rows; ++r)
-        out.ptr[r + 1] = out.ptr[r] + (a.ptr[perm_rows[r] + 1] - a.ptr[perm_rows[r]]);
-    out.idx.resize(a.idx.size());
-    out.val.resize(a.val.size());
-    for (int r = 0; r < rows; ++r) {
-        int q = out.ptr[r];
-        for (int e = a.ptr[perm_rows[r]]; e < a.ptr[perm_rows[r] + 1]; ++e, ++q) {
-            out.idx[q] = inv_cols[a.idx[e]];
-            out.val[q] = a.val[e];
-        }
+// exclusive scan of len[0..rows) into out[0..rows] (len[rows] must be 0)
+void scan_lengths(int* len, int rows, int* out, void*& tmp, size_t& tmp_bytes, Scratch& sc,
+                  cudaStream_t s) {
+    size_t need = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, len, out, rows + 1, s));
+    if (need > tmp_bytes) {
+        tmp = sc.alloc<char>(need);
+        tmp_bytes = need;
     }
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, out, rows + 1, s));
 }
 
-// Twin folding (hpr_update.cuh): consecutive inequality rows with the same
-// pattern and exactly negated coefficients are stored once.
-void fold_twins(int m, int n, int n_eq, const HostCsr& a, const HostCsr& at,
-                std::vector<int32_t>& frow, HostCsr& f, HostCsr& ft) {
-    std::vector<int32_t> fold_of(m), second(m, 0);
-    frow.clear();
-    for (int i = 0; i < m;) {
-        bool pair = false;
-        if (i >= n_eq && i + 1 < m) {
-            const int b0 = a.ptr[i], l0 = a.ptr[i + 1] - b0;
-            const int b1 = a.ptr[i + 1], l1 = a.ptr[i + 2] - b1;
-            if (l0 == l1 && l0 > 0) {
-                pair = true;
-                for (int k = 0; k < l0 && pair; ++k)
-                    pair = a.idx[b0 + k] == a.idx[b1 + k] && a.val[b1 + k] == -a.val[b0 + k];
-            }
-        }
-        fold_of[i] = (int)frow.size();
-        if (pair) {
-            fold_of[i + 1] = (int)frow.size();
-            second[i + 1] = 1;
-        }
-        frow.push_back(i);
-        i += pair ? 2 : 1;
+// stable sort of (key, value) int pairs; returns sorted values in vals_out
+void sort_pairs(const int* keys_in, int* keys_out, const int* vals_in, int* vals_out, long long n,
+                int end_bit, void*& tmp, size_t& tmp_bytes, Scratch& sc, cudaStream_t s) {
+    if (n <= 0) return;
+    size_t need = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in, keys_out, vals_in, vals_out,
+                                       (int)n, 0, end_bit, s));
+    if (need > tmp_bytes) {
+        tmp = sc.alloc<char>(need);
+        tmp_bytes = need;
     }
-    const int nf = (int)frow.size();
-    frow.push_back(m);
-    f.ptr.assign(nf + 1, 0);
-    for (int q = 0; q < nf; ++q) f.ptr[q + 1] = f.ptr[q] + (a.ptr[frow[q] + 1] - a.ptr[frow[q]]);
-    f.idx.resize(f.ptr[nf]);
-    f.val.resize(f.ptr[nf]);
-    f.src.resize(f.ptr[nf]);
-    for (int q = 0; q < nf; ++q) {
-        int o = f.ptr[q];
-        for (int e = a.ptr[frow[q]]; e < a.ptr[frow[q] + 1]; ++e, ++o) {
-            f.idx[o] = a.idx[e];
-            f.val[o] = a.val[e];
-            f.src[o] = e;
-        }
-    }
-    ft.ptr.assign(n + 1, 0);
-    ft.idx.clear();
-    ft.val.clear();
-    ft.src.clear();
-    ft.idx.reserve(f.idx.size());
-    ft.val.reserve(f.idx.size());
-    ft.src.reserve(f.idx.size());
-    for (int j = 0; j < n; ++j) {
-        for (int e = at.ptr[j]; e < at.ptr[j + 1]; ++e) {
-            const int i = at.idx[e];
-            if (second[i]) continue;
-            ft.idx.push_back(fold_of[i]);
-            ft.val.push_back(at.val[e]);
-            ft.src.push_back(e);
-        }
-        ft.ptr[j + 1] = (int32_t)ft.idx.size();
-    }
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, vals_out,
+                                       (int)n, 0, end_bit, s));
+}
+
+int bits_for(long long v) {
+    int b = 1;
+    while (b < 32 && (1LL << b) <= v) ++b;
+    return b;
 }
 
 template <typename T>
@@ -994,36 +951,37 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     CK(cudaStreamSynchronize(s));
 }
 
-void upload_csr(hpr_handle* h, DevCsr& M, const HostCsr& c, int rows, int cols, const Plan& pl,
-                bool with_src) {
-    cudaStream_t s = h->stream;
-    M.rows = rows;
-    M.cols = cols;
-    M.nnz = c.idx.size();
-    M.ntiles = (int)pl.tiles.size();
-    M.nlong = (int)pl.longs.size();
-    CK(cudaMemcpyAsync(M.ptr, c.ptr.data(), sizeof(int) * (rows + 1), cudaMemcpyHostToDevice, s));
-    if (M.nnz) {
-        CK(cudaMemcpyAsync(M.idx, c.idx.data(), sizeof(int) * M.nnz, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(M.mval, c.val.data(), sizeof(double) * M.nnz, cudaMemcpyHostToDevice, s));
-        if (with_src)
-            CK(cudaMemcpyAsync(M.src, c.src.data(), sizeof(int) * M.nnz, cudaMemcpyHostToDevice, s));
-    }
-    CK(cudaMemcpyAsync(M.tiles, pl.tiles.data(), sizeof(int4) * pl.tiles.size(), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(M.taux, pl.taux.data(), sizeof(int2) * pl.taux.size(), cudaMemcpyHostToDevice, s));
-    if (!pl.longs.empty()) {
-        CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
-    }
-    // the host buffers must outlive the async copies
-    CK(cudaStreamSynchronize(s));
-}
-
 void check_plan(const Plan& p, long long rows, long long nnz) {
     const TileBound b = tile_bound(rows, nnz);
     if (p.tiles.size() > b.tiles || p.longs.size() > b.longs)
         fail(HPR_ERR_INVALID, "internal: tile bound violated");
 }
+
+// host tile plan from the device indptr, then the chunk run flags on device
+void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz) {
+    cudaStream_t s = h->stream;
+    std::vector<int32_t> ptr(rows + 1);
+    CK(cudaMemcpyAsync(ptr.data(), M.ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    Plan pl = build_tiles(ptr.data(), rows);
+    check_plan(pl, rows, std::max<long long>(nnz, 1));
+    M.rows = rows;
+    M.cols = cols;
+    M.nnz = nnz;
+    M.ntiles = (int)pl.tiles.size();
+    M.nlong = (int)pl.longs.size();
+    CK(cudaMemcpyAsync(M.tiles, pl.tiles.data(), sizeof(int4) * pl.tiles.size(), cudaMemcpyHostToDevice, s));
+    if (!pl.longs.empty()) {
+        CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
+    }
+    if (M.ntiles)
+        k_chunk_aux<<<nblk((long long)M.ntiles * 32, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(
+            M.tiles, M.ntiles, M.idx, M.taux);
+    CKL();
+    CK(cudaStreamSynchronize(s));   // the host plan must outlive the copies
+}
+
 
 }  // namespace
 
@@ -1065,6 +1023,15 @@ void hpr_destroy(hpr_handle* h);
 
 int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
     hpr_handle* h = nullptr;
+    const bool verbose = getenv("HPR_VERBOSE") != nullptr;
+    auto tp = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (!verbose) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[hpr_create] %-14s %8.1f ms\n", name,
+                std::chrono::duration<double, std::milli>(now - tp).count());
+        tp = now;
+    };
     try {
         validate(p);
         if (!out) fail(HPR_ERR_INVALID, "out is NULL");
@@ -1081,65 +1048,10 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         h->n_eq = p->n_eq;
         h->nnz = p->nnz;
         h->offset = p->offset;
-        const int m = p->m, n = p->n;
-        HostCsr a;
-        a.ptr = to_host(p->indptr, (size_t)m + 1);
-        if (a.ptr[0] != 0 || a.ptr[m] != p->nnz) fail(HPR_ERR_INVALID, "indptr inconsistent with nnz");
-        a.idx = to_host(p->indices, (size_t)p->nnz);
-        a.val = to_host(p->data, (size_t)p->nnz);
-        for (int i = 0; i < m; ++i)
-            if (a.ptr[i + 1] < a.ptr[i]) fail(HPR_ERR_INVALID, "indptr not monotone");
-        for (auto c : a.idx)
-            if (c < 0 || c >= n) fail(HPR_ERR_INVALID, "column index out of range");
-        HostCsr at;
-        if (p->t_indptr && p->t_indices && p->t_data) {
-            at.ptr = to_host(p->t_indptr, (size_t)n + 1);
-            at.idx = to_host(p->t_indices, (size_t)p->nnz);
-            at.val = to_host(p->t_data, (size_t)p->nnz);
-        } else {
-            host_transpose(m, n, a, at);
-        }
+        const int m = p->m, n = p->n, n_eq = p->n_eq;
+        const long long nnz = p->nnz;
         const int flags = opt ? opt->flags : 0;
-        std::vector<int32_t> rperm, cperm;
-        if (!(flags & HPR_FLAG_NO_REORDER)) {
-            compute_order(m, n, p->n_eq, a, rperm, cperm);
-            std::vector<int32_t> rinv(m), cinv(n);
-            for (int i = 0; i < m; ++i) rinv[rperm[i]] = i;
-            for (int j = 0; j < n; ++j) cinv[cperm[j]] = j;
-            HostCsr t1, t2;
-            permute_csr(m, a, rperm, cinv, t1);
-            permute_csr(n, at, cperm, rinv, t2);
-            a.ptr.swap(t1.ptr);
-            a.idx.swap(t1.idx);
-            a.val.swap(t1.val);
-            at.ptr.swap(t2.ptr);
-            at.idx.swap(t2.idx);
-            at.val.swap(t2.val);
-            h->reordered = true;
-        }
-        std::vector<int32_t> frow;
-        HostCsr f, ft;
-        if (!(flags & HPR_FLAG_NO_FOLD)) fold_twins(m, n, p->n_eq, a, at, frow, f, ft);
-        h->nf = frow.empty() ? m : (int)frow.size() - 1;
-        h->folded = h->nf < m;
-        if (!h->folded) {
-            frow.resize(m + 1);
-            for (int i = 0; i <= m; ++i) frow[i] = i;
-            f = a;
-            ft = at;
-            f.src.clear();
-            ft.src.clear();
-        }
-        h->nnz_f = (long long)f.idx.size();
-        const bool runs = !(flags & HPR_FLAG_NO_RUNS);
-        Plan pa = build_tiles(a.ptr.data(), m, runs ? a.idx.data() : nullptr);
-        Plan pt = build_tiles(at.ptr.data(), n, runs ? at.idx.data() : nullptr);
-        Plan pf = build_tiles(f.ptr.data(), h->nf, runs ? f.idx.data() : nullptr);
-        Plan pft = build_tiles(ft.ptr.data(), n, runs ? ft.idx.data() : nullptr);
-        check_plan(pa, m, p->nnz);
-        check_plan(pt, n, p->nnz);
-        check_plan(pf, m, p->nnz);
-        check_plan(pft, n, p->nnz);
+        // workspace (sized from m, n, nnz alone) and streams
         const size_t need = carve(h, nullptr);
         if (opt && opt->workspace) {
             if (opt->workspace_bytes < need) fail(HPR_ERR_NOMEM, "workspace too small");
@@ -1162,28 +1074,202 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
         cudaStream_t s = h->stream;
-        upload_csr(h, h->A, a, m, n, pa, false);
-        upload_csr(h, h->AT, at, n, m, pt, false);
-        upload_csr(h, h->F, f, h->nf, n, pf, h->folded);
-        upload_csr(h, h->FT, ft, n, h->nf, pft, h->folded);
-        CK(cudaMemcpyAsync(h->frow, frow.data(), sizeof(int) * frow.size(), cudaMemcpyHostToDevice, s));
+        Scratch sc;
+        sc.s = s;
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        auto g32 = [](long long items) { return nblk(items * 32, LAYOUT_TPB); };
+
+        // ---- raw CSR on the device (caller's device arrays are used in place)
+        auto on_device = [](const void* q) {
+            cudaPointerAttributes at;
+            const bool d = cudaPointerGetAttributes(&at, q) == cudaSuccess &&
+                           at.type == cudaMemoryTypeDevice;
+            cudaGetLastError();
+            return d;
+        };
+        const int* rptr = p->indptr;
+        const int* ridx = p->indices;
+        const double* rval = p->data;
+        if (!on_device(p->indptr)) {
+            int* q = sc.alloc<int>(m + 1);
+            CK(cudaMemcpyAsync(q, p->indptr, sizeof(int) * (m + 1), cudaMemcpyHostToDevice, s));
+            rptr = q;
+        }
+        if (nnz && !on_device(p->indices)) {
+            int* q = sc.alloc<int>(nnz);
+            upload_pageable(q, p->indices, sizeof(int) * nnz, s);
+            ridx = q;
+        }
+        if (nnz && !on_device(p->data)) {
+            double* q = sc.alloc<double>(nnz);
+            upload_pageable(q, p->data, sizeof(double) * nnz, s);
+            rval = q;
+        }
         {
-            std::vector<int32_t> rmap(m);
-            for (int f = 0; f < h->nf; ++f)
-                for (int i = frow[f]; i < frow[f + 1]; ++i) rmap[i] = 2 * f + (i > frow[f] ? 1 : 0);
-            CK(cudaMemcpyAsync(h->rmap, rmap.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+            int* bad = sc.alloc<int>(4);
+            CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+            k_check_csr<<<std::min(nblk(nnz + m, LAYOUT_TPB), 148 * 32), LAYOUT_TPB, 0, s>>>(
+                rptr, m, ridx, nnz, n, bad);
+            CKL();
+            int hv[3] = {0, 0, 0};
+            CK(cudaMemcpyAsync(&hv[0], bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&hv[1], rptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&hv[2], rptr + m, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            if (hv[1] != 0 || hv[2] != nnz) fail(HPR_ERR_INVALID, "indptr inconsistent with nnz");
+            if (hv[0] & 1) fail(HPR_ERR_INVALID, "column index out of range");
+            if (hv[0] & 2) fail(HPR_ERR_INVALID, "indptr not monotone");
         }
-        if (h->reordered) {
-            CK(cudaMemcpyAsync(h->rperm, rperm.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(h->cperm, cperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        phase("stage+check");
+
+        // ---- A^T: stable sort of the entries by column (rows stay ordered)
+        int* iota_e = sc.alloc<int>(nnz);
+        k_iota<<<nblk(nnz, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(iota_e, (int)nnz, 0);
+        int* row_of = sc.alloc<int>(nnz);
+        k_expand_rows<<<g32(m), LAYOUT_TPB, 0, s>>>(rptr, m, row_of);
+        int* keys_out = sc.alloc<int>(nnz);
+        int* perm_e = sc.alloc<int>(nnz);
+        sort_pairs(ridx, keys_out, iota_e, perm_e, nnz, bits_for(n), tmp, tmp_bytes, sc, s);
+        int* tptr0 = sc.alloc<int>(n + 1);
+        int* tidx0 = sc.alloc<int>(nnz);
+        double* tval0 = sc.alloc<double>(nnz);
+        {
+            int* cnt = sc.alloc<int>(n + 1);
+            CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), s));
+            k_col_count<<<std::min(nblk(nnz, LAYOUT_TPB), 148 * 32), LAYOUT_TPB, 0, s>>>(ridx, nnz, cnt);
+            scan_lengths(cnt, n, tptr0, tmp, tmp_bytes, sc, s);
+            k_take<int><<<std::min(nblk(nnz, LAYOUT_TPB), 148 * 32), LAYOUT_TPB, 0, s>>>(tidx0, row_of, perm_e, nnz);
+            k_take<double><<<std::min(nblk(nnz, LAYOUT_TPB), 148 * 32), LAYOUT_TPB, 0, s>>>(tval0, rval, perm_e, nnz);
+            CKL();
         }
+        phase("transpose");
+
+        // ---- locality ordering + relabelled A, A^T
+        int* rinv = sc.alloc<int>(m);
+        int* cinv = sc.alloc<int>(n);
+        int* lenbuf = sc.alloc<int>(std::max(m, n) + 1);
+        if (!(flags & HPR_FLAG_NO_REORDER)) {
+            int* ckey = sc.alloc<int>(n);
+            k_fill_int<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(ckey, n, 0x7fffffff);
+            k_col_key<<<g32(m), LAYOUT_TPB, 0, s>>>(rptr, ridx, m, LONG_ROW, ckey);
+            int* iota_n = sc.alloc<int>(std::max(m, n));
+            k_iota<<<nblk(std::max(m, n), LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(iota_n, std::max(m, n), 0);
+            int* kout = sc.alloc<int>(std::max(m, n));
+            sort_pairs(ckey, kout, iota_n, h->cperm, n, 32, tmp, tmp_bytes, sc, s);
+            k_invert<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->cperm, n, cinv);
+            int* rkey = sc.alloc<int>(m);
+            k_row_key<<<g32(m), LAYOUT_TPB, 0, s>>>(rptr, ridx, m, cinv, rkey);
+            sort_pairs(rkey, kout, iota_n, h->rperm, n_eq, 32, tmp, tmp_bytes, sc, s);
+            sort_pairs(rkey + n_eq, kout, iota_n + n_eq, h->rperm + n_eq, m - n_eq, 32, tmp,
+                       tmp_bytes, sc, s);
+            k_invert<<<nblk(m, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->rperm, m, rinv);
+            CKL();
+            h->reordered = true;
+        } else {
+            k_iota<<<nblk(m, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->rperm, m, 0);
+            k_iota<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->cperm, n, 0);
+            k_iota<<<nblk(m, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(rinv, m, 0);
+            k_iota<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(cinv, n, 0);
+            CKL();
+        }
+        CK(cudaMemsetAsync(lenbuf + m, 0, sizeof(int), s));
+        k_perm_len<<<nblk(m, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(rptr, h->rperm, m, lenbuf);
+        scan_lengths(lenbuf, m, h->A.ptr, tmp, tmp_bytes, sc, s);
+        k_gather_rows<<<g32(m), LAYOUT_TPB, 0, s>>>(rptr, ridx, rval, h->rperm, m, h->A.ptr, cinv,
+                                                     h->A.idx, h->A.mval, nullptr);
+        CK(cudaMemsetAsync(lenbuf + n, 0, sizeof(int), s));
+        k_perm_len<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(tptr0, h->cperm, n, lenbuf);
+        scan_lengths(lenbuf, n, h->AT.ptr, tmp, tmp_bytes, sc, s);
+        k_gather_rows<<<g32(n), LAYOUT_TPB, 0, s>>>(tptr0, tidx0, tval0, h->cperm, n, h->AT.ptr,
+                                                     rinv, h->AT.idx, h->AT.mval, nullptr);
+        CKL();
+        phase("reorder");
+
+        // ---- twin folding (pairing decided on the host from device candidates)
+        std::vector<int32_t> frow;
+        std::vector<unsigned char> second(m, 0);
+        if (!(flags & HPR_FLAG_NO_FOLD) && m > 1) {
+            unsigned char* cand = sc.alloc<unsigned char>(m);
+            k_twin_candidates<<<g32(m), LAYOUT_TPB, 0, s>>>(h->A.ptr, h->A.idx, h->A.mval, m,
+                                                             n_eq, cand);
+            CKL();
+            std::vector<unsigned char> hc(m);
+            CK(cudaMemcpyAsync(hc.data(), cand, m, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (int i = 0; i < m;) {
+                frow.push_back(i);
+                if (hc[i]) {
+                    second[i + 1] = 1;
+                    i += 2;
+                } else {
+                    i += 1;
+                }
+            }
+        } else {
+            frow.resize(m);
+            for (int i = 0; i < m; ++i) frow[i] = i;
+        }
+        h->nf = (int)frow.size();
+        frow.push_back(m);
+        h->folded = h->nf < m;
+        std::vector<int32_t> fold_of(m), rmap(m);
+        for (int f = 0; f < h->nf; ++f)
+            for (int i = frow[f]; i < frow[f + 1]; ++i) {
+                fold_of[i] = f;
+                rmap[i] = 2 * f + (i > frow[f] ? 1 : 0);
+            }
+        CK(cudaMemcpyAsync(h->frow, frow.data(), sizeof(int) * frow.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(h->rmap, rmap.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+        if (h->folded) {
+            unsigned char* dsec = sc.alloc<unsigned char>(m);
+            int* dfold = sc.alloc<int>(m);
+            CK(cudaMemcpyAsync(dsec, second.data(), m, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dfold, fold_of.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(lenbuf + h->nf, 0, sizeof(int), s));
+            k_perm_len<<<nblk(h->nf, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->A.ptr, h->frow, h->nf, lenbuf);
+            scan_lengths(lenbuf, h->nf, h->F.ptr, tmp, tmp_bytes, sc, s);
+            k_gather_rows<<<g32(h->nf), LAYOUT_TPB, 0, s>>>(h->A.ptr, h->A.idx, h->A.mval, h->frow,
+                                                             h->nf, h->F.ptr, nullptr, h->F.idx,
+                                                             h->F.mval, h->F.src);
+            CK(cudaMemsetAsync(lenbuf + n, 0, sizeof(int), s));
+            k_fold_count<<<g32(n), LAYOUT_TPB, 0, s>>>(h->AT.ptr, h->AT.idx, n, dsec, lenbuf);
+            scan_lengths(lenbuf, n, h->FT.ptr, tmp, tmp_bytes, sc, s);
+            k_fold_gather<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->AT.ptr, h->AT.idx,
+                                                                     h->AT.mval, n, dsec, dfold,
+                                                                     h->FT.ptr, h->FT.idx,
+                                                                     h->FT.mval, h->FT.src);
+            CKL();
+            int nf_nnz = 0;
+            CK(cudaMemcpyAsync(&nf_nnz, h->F.ptr + h->nf, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            h->nnz_f = nf_nnz;
+        } else {
+            CK(cudaMemcpyAsync(h->F.ptr, h->A.ptr, sizeof(int) * (m + 1), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(h->FT.ptr, h->AT.ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+            if (nnz) {
+                CK(cudaMemcpyAsync(h->F.idx, h->A.idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(h->FT.idx, h->AT.idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(h->F.mval, h->A.mval, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(h->FT.mval, h->AT.mval, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+            }
+            h->nnz_f = nnz;
+        }
+        phase("fold");
+
+        // ---- tile schedules (host plan from the device indptr)
+        plan_tiles(h, h->A, m, n, nnz);
+        plan_tiles(h, h->AT, n, m, nnz);
+        plan_tiles(h, h->F, h->nf, n, h->nnz_f);
+        plan_tiles(h, h->FT, n, h->nf, h->nnz_f);
+        phase("tiles");
         put_vec(h, h->rhs_m, p->rhs, m, true);
         put_vec(h, h->cost_m, p->cost, n, false);
         put_vec(h, h->lo_m, p->lower, n, false);
         put_vec(h, h->up_m, p->upper, n, false);
         CK(cudaMemsetAsync(h->ctrl, 0, sizeof(Ctrl), s));
         CK(cudaStreamSynchronize(s));
+        phase("upload");
         *out = h;
         return HPR_OK;
     } catch (const HprError& e) {

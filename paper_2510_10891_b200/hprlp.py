@@ -219,11 +219,7 @@ class Engine:
         self.n_eq = int(lp.n_eq)
         self.offset = float(getattr(lp, "offset", 0.0))
         self._keep = [_i32(csr.indptr), _i32(csr.indices), _f64(csr.data)]
-        csc = getattr(lp.matrix, "csc", None)
-        tparts = [None, None, None]
-        if csc is not None and csc.has_sorted_indices and csc.nnz == csr.nnz:
-            tparts = [_i32(csc.indptr), _i32(csc.indices), _f64(csc.data)]
-            self._keep += tparts
+        tparts = [None, None, None]          # A^T is built on the device (hpr_layout.cuh)
         vecs = [_f64(lp.rhs), _f64(lp.cost), _f64(lp.lower), _f64(lp.upper)]
         if vecs[0].shape != (m,) or any(v.shape != (n,) for v in vecs[1:]):
             raise ValueError("LP vector lengths do not match the matrix shape")
