@@ -77,7 +77,8 @@ typedef struct hpr_problem {
 
 #define HPR_FLAG_NO_REORDER 1  /* keep the caller's row/column order on the device */
 #define HPR_FLAG_NO_FOLD 2     /* do not merge twin (x, -x) inequality rows */
-#define HPR_FLAG_NO_RUNS 4     /* keep explicit column indices for dense long-row chunks */
+#define HPR_FLAG_NO_RUNS 4     /* read every column index (no index-free long-row chunks) */
+#define HPR_FLAG_NO_PANELS 8   /* keep the dense flow blocks in F^T (no A^T y panels from F) */
 
 typedef struct hpr_options {
     int32_t device;            /* CUDA ordinal */
@@ -213,6 +214,11 @@ typedef struct hpr_layout {
     int32_t tiles_a, tiles_at, tiles_f, tiles_ft;
     int32_t reordered, folded;
     size_t workspace_bytes;
+    int64_t panel_cols;        /* columns whose dense flow block is read from F (A^T y panels) */
+    int64_t panel_nnz;         /* entries of F^T served by those panels (dropped from F^T) */
+    int64_t f_nnz;             /* entries of F incl. explicit zeros padding flow rows */
+    int64_t ft_nnz;            /* entries left in F^T */
+    int64_t index_free_nnz_f;  /* entries of F streamed without their column index */
 } hpr_layout;
 int hpr_get_layout(hpr_handle* h, hpr_layout* out);
 

@@ -21,6 +21,7 @@ HPR_FP64, HPR_FP32 = 0, 1
 HPR_FLAG_NO_REORDER = 1
 HPR_FLAG_NO_FOLD = 2
 HPR_FLAG_NO_RUNS = 4
+HPR_FLAG_NO_PANELS = 8
 HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",
@@ -86,7 +87,9 @@ class Layout(C.Structure):
                 ("folded_rows", C.c_int32), ("nnz", C.c_int64), ("folded_nnz", C.c_int64),
                 ("tiles_a", C.c_int32), ("tiles_at", C.c_int32), ("tiles_f", C.c_int32),
                 ("tiles_ft", C.c_int32), ("reordered", C.c_int32), ("folded", C.c_int32),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("panel_cols", C.c_int64),
+                ("panel_nnz", C.c_int64), ("f_nnz", C.c_int64), ("ft_nnz", C.c_int64),
+                ("index_free_nnz_f", C.c_int64)]
 
 
 class HprError(RuntimeError):

@@ -84,6 +84,17 @@ struct Csr {
     int* counters;           // per long row, zero between launches
     double* tile_part;       // per tile partial sums of long-row chunks (work dtype)
     const int2* taux;        // per tile {c0, 1} if the chunk's columns are c0, c0+1, ...; else {0, 0}
+    // flow panels (F^T only; hpr_layout.cuh k_col_panels): row r's dense flow
+    // part is sum_q pvals[rbase[i0+q] + r] * x[i0+q], {i0, L} = pinfo[r]
+    const T* pvals;
+    const int2* pinfo;
+    const int* rbase;
+    // per panel tile {i0, L, base, stride}: all its rows share the panel rows
+    // i0 .. i0+L-1 and those F rows form one row-major block, so
+    // F(i0+q, r) = pvals[base + q*stride + r] (stride 0: use pinfo / rbase)
+    const int4* pdesc;
 };
+
+constexpr int PANEL_ROWS = 32;    // rows (F^T columns) per panel tile: one warp-width
 
 }  // namespace hpr

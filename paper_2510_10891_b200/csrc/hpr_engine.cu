@@ -67,7 +67,22 @@ static void fail(int code, const std::string& msg) {
             fail(HPR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
     } while (0)
 
-#define CKL() CK(cudaGetLastError())
+// HPR_SYNC_DEBUG=1: synchronise after every launch outside graph capture and
+// run the solve loop eagerly, so a faulting kernel is named in the error.
+static bool sync_debug() {
+    static const bool on = getenv("HPR_SYNC_DEBUG") != nullptr;
+    return on;
+}
+static thread_local bool g_capturing = false;
+
+static void ck_last(int line) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && sync_debug() && !g_capturing) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+        fail(HPR_ERR_CUDA, "hpr_engine.cu:" + std::to_string(line) + ": " + cudaGetErrorString(e));
+}
+
+#define CKL() ck_last(__LINE__)
 
 namespace {
 
@@ -82,8 +97,13 @@ void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&.
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.stream = s;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-    if (e != cudaSuccess) fail(HPR_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e == cudaSuccess && sync_debug() && !g_capturing) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        const char* name = "?";
+        cudaFuncGetName(&name, (const void*)kern);
+        fail(HPR_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+    }
 }
 
 // fixed grid of the row-wise passes: deterministic partial-sum slots
@@ -99,11 +119,27 @@ struct Plan {
 };
 
 // Cut a CSR into stream tiles and long-row chunks (see hpr_spmv.cuh).
-Plan build_tiles(const int32_t* ptr, int rows) {
+Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr) {
     Plan p;
     int r = 0;
+    auto panel = [&](int q) { return pinfo && pinfo[q].y > 0; };
+    auto same = [&](int a, int b) { return pinfo[a].x == pinfo[b].x && pinfo[a].y == pinfo[b].y; };
     while (r < rows) {
         const int len = ptr[r + 1] - ptr[r];
+        if (panel(r)) {
+            // panel tile: consecutive panel rows, remaining entries staged like a stream tile
+            const int r0 = r;
+            long long nz = 0;
+            while (r < rows && r - r0 < PANEL_ROWS && panel(r) && same(r, r0)) {
+                const int l = ptr[r + 1] - ptr[r];
+                if (nz + l > TILE_NNZ) break;
+                nz += l;
+                ++r;
+            }
+            if (r == r0) fail(HPR_ERR_INVALID, "internal: panel row too long");
+            p.tiles.push_back(make_int4(r0, -(r + 1), ptr[r0], -(ptr[r] + 1)));
+            continue;
+        }
         if (len > TILE_NNZ) {
             const int li = (int)p.longs.size();
             const int nch = (len + CHUNK_NNZ - 1) / CHUNK_NNZ;
@@ -118,7 +154,7 @@ Plan build_tiles(const int32_t* ptr, int rows) {
         }
         const int r0 = r;
         long long nz = 0;
-        while (r < rows && r - r0 < TILE_ROWS) {
+        while (r < rows && r - r0 < TILE_ROWS && !panel(r)) {
             const int l = ptr[r + 1] - ptr[r];
             if (l > TILE_NNZ || nz + l > TILE_NNZ) break;
             nz += l;
@@ -136,10 +172,11 @@ Plan build_tiles(const int32_t* ptr, int rows) {
 struct TileBound {
     size_t tiles, longs;
 };
-TileBound tile_bound(long long rows, long long nnz) {
+TileBound tile_bound(long long rows, long long nnz, bool panels = false) {
     const long long nlong = std::min<long long>(rows, nnz / (TILE_NNZ + 1));
+    // panel runs (F^T) cut stream tiles: at most one extra tile per row
     const long long t = 2 * (nnz / TILE_NNZ + 1) + rows / TILE_ROWS + 1 + 2 * nlong +
-                        (nnz / CHUNK_NNZ + 1) + nlong + 2;
+                        (nnz / CHUNK_NNZ + 1) + nlong + 2 + (panels ? rows + 1 : 0);
     return {(size_t)t, (size_t)std::max<long long>(nlong, 1)};
 }
 
@@ -167,11 +204,15 @@ struct DevCsr {
     int* src = nullptr;          // folded operands: source entry in the unfolded values
     int4 *tiles = nullptr, *longs = nullptr;
     int2* taux = nullptr;
+    const int2* pinfo = nullptr;  // flow panels (F^T only)
+    const int* rbase = nullptr;
+    int4* pdesc = nullptr;        // per tile (hpr_common.cuh Csr::pdesc)
     int ntiles = 0, nlong = 0;
+    long long free_nnz = 0;      // entries in index-free chunks
     int* counters = nullptr;
     double* tpart = nullptr;
     template <typename T>
-    Csr<T> view(const T* vals) const {
+    Csr<T> view(const T* vals, const T* pvals = nullptr) const {
         Csr<T> c;
         c.rows = rows;
         c.cols = cols;
@@ -185,6 +226,10 @@ struct DevCsr {
         c.counters = counters;
         c.tile_part = tpart;
         c.taux = taux;
+        c.pvals = pvals;
+        c.pinfo = pinfo;
+        c.rbase = rbase;
+        c.pdesc = pdesc;
         return c;
     }
     int nslots() const { return ntiles + nlong; }
@@ -201,6 +246,11 @@ struct hpr_handle {
     bool folded = false;
     int* frow = nullptr;                     // nf + 1 folded-row starts
     int* rmap = nullptr;                     // m: 2 * folded row + second-of-pair
+    // flow panels (hpr_layout.cuh): the dense flow block of A^T y read from F
+    bool panels = false;
+    int2* pinfo = nullptr;                   // n: {first folded row, count}
+    int* rbase = nullptr;                    // folded rows: F entry of column 0 (INT_MIN: not dense)
+    long long panel_nnz = 0, panel_cols = 0;
     // vectors (engine order)
     double *rhs_m, *cost_m, *lo_m, *up_m, *rs, *cs, *fr, *fc;
     double *rhs_w, *cost_w, *lo_w, *up_w;    // FP64 work (setup)
@@ -225,6 +275,7 @@ struct hpr_handle {
     cudaGraphExec_t gexec = nullptr;
     unsigned long long gcond = 0;
     int g_B = 0, g_prec = -1;
+    LogRec* g_log = nullptr;
     long long g_per_block = 0;
     int last_prec = -1;
     bool reordered = false;
@@ -233,6 +284,7 @@ struct hpr_handle {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
     int* d_flag = nullptr;                   // collective stop flag (time limit)
+    int flags = 0;                           // hpr_options.flags
 };
 
 namespace {
@@ -245,7 +297,7 @@ size_t carve(hpr_handle* h, char* base) {
     Carver cv;
     cv.base = base;
     const size_t m = h->m, n = h->n, nnz = h->nnz;
-    const TileBound bm = tile_bound(m, nnz), bn = tile_bound(n, nnz);
+    const TileBound bm = tile_bound(m, nnz), bn = tile_bound(n, nnz, true);
     auto csr = [&](DevCsr& M, size_t rows, const TileBound& tb, bool work32, bool src) {
         M.ptr = cv.take<int>(rows + 1);
         M.idx = cv.take<int>(nnz);
@@ -258,6 +310,7 @@ size_t carve(hpr_handle* h, char* base) {
         M.counters = cv.take<int>(tb.longs);
         M.tpart = cv.take<double>(tb.tiles);
         M.taux = cv.take<int2>(tb.tiles);
+        M.pdesc = &M == &h->FT ? cv.take<int4>(tb.tiles) : nullptr;
     };
     csr(h->A, m, bm, false, false);
     csr(h->AT, n, bn, false, false);
@@ -265,6 +318,8 @@ size_t carve(hpr_handle* h, char* base) {
     csr(h->FT, n, bn, true, true);
     h->frow = cv.take<int>(m + 1);
     h->rmap = cv.take<int>(m);
+    h->pinfo = cv.take<int2>(n);
+    h->rbase = cv.take<int>(m);
     for (double** v : {&h->rhs_m, &h->rs, &h->fr, &h->rhs_w, &h->YM, &h->YMF, &h->BYm})
         *v = cv.take<double>(m);
     for (double** v : {&h->cost_m, &h->lo_m, &h->up_m, &h->cs, &h->fc, &h->cost_w, &h->lo_w,
@@ -303,6 +358,8 @@ size_t carve(hpr_handle* h, char* base) {
 // stays the original one, so every row sum keeps the reference's summation
 // order; only the labels move.
 constexpr int LONG_ROW = 256;
+constexpr int PANEL_MIN_ROW = 256;   // dense F rows that can serve a panel (PTDF flow rows)
+constexpr int PANEL_MIN_RUN = 8;     // consecutive flow rows per column worth a panel
 
 // scratch owned by one hpr_create call (stream-ordered pool allocations)
 struct Scratch {
@@ -464,8 +521,9 @@ double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only,
 
 template <typename T, class Epi>
 void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, const Epi& epi,
-                 cudaStream_t s) {
-    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, M.view<T>(vals), xg, epi);
+                 cudaStream_t s, const T* pvals = nullptr) {
+    if (M.pinfo && !pvals) fail(HPR_ERR_INVALID, "internal: panel operand without F values");
+    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, M.view<T>(vals, pvals), xg, epi);
     h->launches += 1;
 }
 
@@ -528,18 +586,13 @@ double power_method(hpr_handle* h, const double* a_vals, const double* at_vals, 
 // copy the scaled unfolded values into the folded operands
 void refresh_folded_values(hpr_handle* h, bool fp32) {
     cudaStream_t s = h->stream;
-    if (h->folded) {
-        k_gather_vals<<<nblk(h->nnz_f), TPB, 0, s>>>(h->F.w64, h->A.w64, h->F.src, h->nnz_f);
-        k_gather_vals<<<nblk(h->nnz_f), TPB, 0, s>>>(h->FT.w64, h->AT.w64, h->FT.src, h->nnz_f);
-        CKL();
-        h->launches += 2;
-    } else {
-        CK(cudaMemcpyAsync(h->F.w64, h->A.w64, sizeof(double) * h->nnz, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(h->FT.w64, h->AT.w64, sizeof(double) * h->nnz, cudaMemcpyDeviceToDevice, s));
-    }
+    k_gather_vals<<<nblk(h->F.nnz), TPB, 0, s>>>(h->F.w64, h->A.w64, h->F.src, h->F.nnz);
+    k_gather_vals<<<nblk(h->FT.nnz), TPB, 0, s>>>(h->FT.w64, h->AT.w64, h->FT.src, h->FT.nnz);
+    CKL();
+    h->launches += 2;
     if (fp32) {
-        k_cast_f32<<<nblk(h->nnz_f), TPB, 0, s>>>(h->F.w64, h->F.w32, h->nnz_f);
-        k_cast_f32<<<nblk(h->nnz_f), TPB, 0, s>>>(h->FT.w64, h->FT.w32, h->nnz_f);
+        k_cast_f32<<<nblk(h->F.nnz), TPB, 0, s>>>(h->F.w64, h->F.w32, h->F.nnz);
+        k_cast_f32<<<nblk(h->FT.nnz), TPB, 0, s>>>(h->FT.w64, h->FT.w32, h->FT.nnz);
         CKL();
         h->launches += 2;
     }
@@ -653,7 +706,8 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     launch(k_check_rows<T>, gr, TPB, s, ar);
     allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
-    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s,
+                (const double*)h->F.mval);
     allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
     CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                         h->colpart};
@@ -671,7 +725,7 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
 template <typename T, bool CHECK>
 void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
     EpiStore<T> st{p.P, nullptr};
-    launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s);                       // A^T y
+    launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals);             // A^T y
     allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs};
@@ -692,7 +746,8 @@ void enqueue_iteration(hpr_handle* h, const Ptrs<T>& p, int j, bool check, cudaS
 template <typename T>
 void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     const int prec = sizeof(T) == 4 ? HPR_FP32 : HPR_FP64;
-    if (h->gexec && h->g_B == B && h->g_prec == prec) return;
+    // the log buffer is a captured kernel argument: a reallocation needs a new graph
+    if (h->gexec && h->g_B == B && h->g_prec == prec && h->g_log == h->log) return;
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
     if (h->graph) cudaGraphDestroy(h->graph);
     h->gexec = nullptr;
@@ -717,14 +772,17 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     const long long l0 = h->launches;
     CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
+    g_capturing = true;
     try {
         for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
         enqueue_check<T>(h, p, 1, h->cap);
     } catch (...) {
+        g_capturing = false;
         cudaGraph_t dummy;
         cudaStreamEndCapture(h->cap, &dummy);
         throw;
     }
+    g_capturing = false;
     cudaGraph_t captured;
     CK(cudaStreamEndCapture(h->cap, &captured));
     h->g_per_block = h->launches - l0;
@@ -733,6 +791,7 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     h->gcond = (unsigned long long)cond;
     h->g_B = B;
     h->g_prec = prec;
+    h->g_log = h->log;
 }
 
 // Launch the cached loop graph from the current device state; returns the
@@ -914,8 +973,20 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
                 CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
             }
         }
-        ensure_graph<T>(h, p, B);
-        st->loop_seconds = run_loop(h, time_left);
+        if (sync_debug() && !h->comm) {
+            // eager block loop (no graph, no deadline): debugging only
+            const auto t0 = std::chrono::steady_clock::now();
+            do {
+                for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, s);
+                enqueue_check<T>(h, p, 1, s);
+                read_ctrl(h);
+            } while (h->h_ctrl->status == -1);
+            st->loop_seconds =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        } else {
+            ensure_graph<T>(h, p, B);
+            st->loop_seconds = run_loop(h, time_left);
+        }
         status = h->h_ctrl->status;
         iterations = h->h_ctrl->total;
         if (status == HPR_ITERATION_LIMIT) iterations = prm->max_iterations;
@@ -951,20 +1022,24 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     CK(cudaStreamSynchronize(s));
 }
 
-void check_plan(const Plan& p, long long rows, long long nnz) {
-    const TileBound b = tile_bound(rows, nnz);
+void check_plan(const Plan& p, long long rows, long long nnz, bool panels) {
+    const TileBound b = tile_bound(rows, nnz, panels);
     if (p.tiles.size() > b.tiles || p.longs.size() > b.longs)
         fail(HPR_ERR_INVALID, "internal: tile bound violated");
 }
 
 // host tile plan from the device indptr, then the chunk run flags on device
-void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz) {
+void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
+                const int2* d_pinfo = nullptr) {
     cudaStream_t s = h->stream;
     std::vector<int32_t> ptr(rows + 1);
+    std::vector<int2> pinfo(d_pinfo ? rows : 0);
     CK(cudaMemcpyAsync(ptr.data(), M.ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost, s));
+    if (d_pinfo && rows)
+        CK(cudaMemcpyAsync(pinfo.data(), d_pinfo, sizeof(int2) * rows, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    Plan pl = build_tiles(ptr.data(), rows);
-    check_plan(pl, rows, std::max<long long>(nnz, 1));
+    Plan pl = build_tiles(ptr.data(), rows, d_pinfo ? pinfo.data() : nullptr);
+    check_plan(pl, rows, std::max<long long>(nnz, 1), &M == &h->FT || &M == &h->AT);
     M.rows = rows;
     M.cols = cols;
     M.nnz = nnz;
@@ -975,10 +1050,40 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz) {
         CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
     }
-    if (M.ntiles)
+    if (d_pinfo && M.ntiles) {
+        // panel tiles over one row-major block of F get a direct descriptor
+        std::vector<int32_t> rb(h->nf);
+        CK(cudaMemcpyAsync(rb.data(), h->rbase, sizeof(int) * h->nf, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<int4> pd(M.ntiles, make_int4(0, 0, 0, 0));
+        for (int t = 0; t < M.ntiles; ++t) {
+            const int4 tl = pl.tiles[t];
+            if (!(tl.y < 0 && tl.w < 0)) continue;
+            const int2 pi = pinfo[tl.x];
+            const long long stride = pi.y > 1 ? (long long)rb[pi.x + 1] - rb[pi.x] : 1;
+            bool uni = stride > 0 && stride < INT_MAX;
+            for (int q = 1; q < pi.y && uni; ++q)
+                uni = (long long)rb[pi.x + q] == (long long)rb[pi.x] + q * stride;
+            if (uni) pd[t] = make_int4(pi.x, pi.y, rb[pi.x], (int)stride);
+        }
+        CK(cudaMemcpyAsync(M.pdesc, pd.data(), sizeof(int4) * M.ntiles, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    const bool runs = !(h->flags & HPR_FLAG_NO_RUNS);
+    if (M.ntiles && runs)
         k_chunk_aux<<<nblk((long long)M.ntiles * 32, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(
             M.tiles, M.ntiles, M.idx, M.taux);
+    else if (M.ntiles)
+        CK(cudaMemsetAsync(M.taux, 0, sizeof(int2) * M.ntiles, s));
     CKL();
+    M.free_nnz = 0;                 // entries streamed without their index (introspection)
+    if (M.ntiles && runs) {
+        std::vector<int2> ta(M.ntiles);
+        CK(cudaMemcpyAsync(ta.data(), M.taux, sizeof(int2) * M.ntiles, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int t = 0; t < M.ntiles; ++t)
+            if (pl.tiles[t].y >= 0 && ta[t].y) M.free_nnz += pl.tiles[t].z - pl.tiles[t].y;
+    }
     CK(cudaStreamSynchronize(s));   // the host plan must outlive the copies
 }
 
@@ -1051,6 +1156,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         const int m = p->m, n = p->n, n_eq = p->n_eq;
         const long long nnz = p->nnz;
         const int flags = opt ? opt->flags : 0;
+        h->flags = flags;
         // workspace (sized from m, n, nnz alone) and streams
         const size_t need = carve(h, nullptr);
         if (opt && opt->workspace) {
@@ -1252,16 +1358,92 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
                 CK(cudaMemcpyAsync(h->FT.idx, h->AT.idx, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, s));
                 CK(cudaMemcpyAsync(h->F.mval, h->A.mval, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
                 CK(cudaMemcpyAsync(h->FT.mval, h->AT.mval, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+                k_iota<<<nblk(nnz, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->F.src, (int)nnz, 0);
+                k_iota<<<nblk(nnz, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(h->FT.src, (int)nnz, 0);
+                CKL();
             }
             h->nnz_f = nnz;
         }
         phase("fold");
 
+        // ---- pad nearly dense flow rows of F to single column runs (explicit
+        // zeros; only while the padded operand fits the carved capacity)
+        long long f_nnz = h->nnz_f;
+        if (!(flags & HPR_FLAG_NO_RUNS) && h->nf && h->nnz_f) {
+            int* plen = sc.alloc<int>(h->nf + 1);
+            CK(cudaMemsetAsync(plen + h->nf, 0, sizeof(int), s));
+            k_pad_count<<<g32(h->nf), LAYOUT_TPB, 0, s>>>(h->F.ptr, h->F.idx, h->nf,
+                                                           PANEL_MIN_ROW, plen);
+            CKL();
+            int* nptr = sc.alloc<int>(h->nf + 1);
+            scan_lengths(plen, h->nf, nptr, tmp, tmp_bytes, sc, s);
+            int tot = 0;
+            CK(cudaMemcpyAsync(&tot, nptr + h->nf, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (tot > h->nnz_f && tot <= nnz) {
+                int* oidx = sc.alloc<int>(h->nnz_f);
+                int* osrc = sc.alloc<int>(h->nnz_f);
+                double* oval = sc.alloc<double>(h->nnz_f);
+                int* optr = sc.alloc<int>(h->nf + 1);
+                CK(cudaMemcpyAsync(optr, h->F.ptr, sizeof(int) * (h->nf + 1), cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(oidx, h->F.idx, sizeof(int) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(osrc, h->F.src, sizeof(int) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(oval, h->F.mval, sizeof(double) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(h->F.ptr, nptr, sizeof(int) * (h->nf + 1), cudaMemcpyDeviceToDevice, s));
+                k_pad_gather<<<g32(h->nf), LAYOUT_TPB, 0, s>>>(optr, oidx, oval, osrc, h->nf,
+                                                                h->F.ptr, h->F.idx, h->F.mval,
+                                                                h->F.src);
+                CKL();
+                f_nnz = tot;
+            }
+        }
+        phase("pad");
+
+        // ---- flow panels: F^T drops the dense flow block, read from F instead
+        // (single GPU: a partitioned solve reduces A^T y over ranks before the update)
+        long long ft_nnz = h->nnz_f;
+        if (!(flags & HPR_FLAG_NO_PANELS) && !h->comm && h->nf && n && h->nnz_f) {
+            k_dense_rows<<<g32(h->nf), LAYOUT_TPB, 0, s>>>(h->F.ptr, h->F.idx, h->nf,
+                                                            PANEL_MIN_ROW, h->rbase);
+            int* roff = sc.alloc<int>(n);
+            CK(cudaMemsetAsync(h->d_dev, 0, 2 * sizeof(unsigned long long), s));
+            CK(cudaMemsetAsync(lenbuf + n, 0, sizeof(int), s));
+            k_col_panels<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(
+                h->FT.ptr, h->FT.idx, n, h->rbase, PANEL_MIN_RUN, TILE_NNZ / PANEL_ROWS, h->pinfo, roff, lenbuf,
+                h->d_dev);
+            CKL();
+            unsigned long long cov[2] = {0, 0};
+            CK(cudaMemcpyAsync(cov, h->d_dev, sizeof(cov), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (cov[0] * 10 >= (unsigned long long)h->nnz_f) {      // worth a layout change
+                int* optr = sc.alloc<int>(n + 1);
+                int* oidx = sc.alloc<int>(h->nnz_f);
+                int* osrc = sc.alloc<int>(h->nnz_f);
+                double* oval = sc.alloc<double>(h->nnz_f);
+                CK(cudaMemcpyAsync(optr, h->FT.ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(oidx, h->FT.idx, sizeof(int) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(osrc, h->FT.src, sizeof(int) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                CK(cudaMemcpyAsync(oval, h->FT.mval, sizeof(double) * h->nnz_f, cudaMemcpyDeviceToDevice, s));
+                scan_lengths(lenbuf, n, h->FT.ptr, tmp, tmp_bytes, sc, s);
+                k_drop_panels<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(
+                    optr, oidx, oval, osrc, n, h->pinfo, roff, h->FT.ptr, h->FT.idx, h->FT.mval,
+                    h->FT.src);
+                CKL();
+                h->panels = true;
+                h->FT.pinfo = h->pinfo;
+                h->FT.rbase = h->rbase;
+                h->panel_nnz = (long long)cov[0];
+                h->panel_cols = (long long)cov[1];
+                ft_nnz = h->nnz_f - h->panel_nnz;
+            }
+        }
+        phase("panels");
+
         // ---- tile schedules (host plan from the device indptr)
         plan_tiles(h, h->A, m, n, nnz);
         plan_tiles(h, h->AT, n, m, nnz);
-        plan_tiles(h, h->F, h->nf, n, h->nnz_f);
-        plan_tiles(h, h->FT, n, h->nf, h->nnz_f);
+        plan_tiles(h, h->F, h->nf, n, f_nnz);
+        plan_tiles(h, h->FT, n, h->nf, ft_nnz, h->panels ? h->pinfo : nullptr);
         phase("tiles");
         put_vec(h, h->rhs_m, p->rhs, m, true);
         put_vec(h, h->cost_m, p->cost, n, false);
@@ -1382,7 +1564,8 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     CheckRowsArgs<double> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     k_check_rows<double><<<gr, TPB, 0, s>>>(ar);
     allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
-    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s);
+    launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s,
+                (const double*)h->F.mval);
     allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
     CheckColsArgs<double> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                              h->colpart};
@@ -1534,6 +1717,11 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
     out->reordered = h->reordered;
     out->folded = h->folded;
     out->workspace_bytes = h->ws_bytes;
+    out->panel_cols = h->panel_cols;
+    out->panel_nnz = h->panel_nnz;
+    out->f_nnz = h->F.nnz;
+    out->ft_nnz = h->FT.nnz;
+    out->index_free_nnz_f = h->F.free_nnz;
     API_END
 }
 
@@ -1588,7 +1776,7 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
                        p.BY, p.BYF, h->YM, h->YMF, h->rs};
         switch (which) {
             case 0: launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s); break;
-            case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s); break;
+            case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals); break;
             case 2: k_update_primal<T, false><<<nblk(h->n), TPB, 0, s>>>(pa); break;
             case 3: k_update_dual<T, false><<<nblk(h->m), TPB, 0, s>>>(da); break;
             default: enqueue_check<T>(h, p, 1, s); break;

@@ -10,6 +10,8 @@
 // Entry order inside every row is preserved through all of it.
 #pragma once
 
+#include <climits>
+
 #include <cub/cub.cuh>
 
 #include "hpr_common.cuh"
@@ -162,6 +164,136 @@ __global__ void k_chunk_aux(const int4* tiles, int ntiles, const int* idx, int2*
     for (int e = tl.y + 1 + lane; e < tl.z; e += 32) run = run && idx[e] == idx[e - 1] + 1;
     run = __all_sync(0xffffffffu, run);
     if (lane == 0) taux[t] = run ? make_int2(idx[tl.y], 1) : make_int2(0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Flow panels.  After the locality ordering a PTDF flow row of F covers one
+// period's columns as a single run (F row i = columns j0 .. j0+len-1), and a
+// column's flow entries in F^T are consecutive folded rows.  The block is
+// dense, so (A^T y)_j's flow part can read F's own row-major values at
+// vals[rbase[i] + j] (rbase[i] = ptr[i] - j0) with y broadcast and the
+// values coalesced across columns — F^T keeps only the remaining entries.
+// ---------------------------------------------------------------------------
+
+// Nearly dense flow rows (a PTDF row misses only the few zero-PTDF columns
+// of its period, e.g. the slack bus) are padded with explicit zeros to one
+// run of consecutive columns, so both products address them index-free.
+// padlen[r] = span when row r (>= min_len entries, strictly increasing
+// columns) misses at most len/32 columns of its span, else its length.
+__global__ void k_pad_count(const int* ptr, const int* idx, int rows, int min_len, int* padlen) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const int b = ptr[w], len = ptr[w + 1] - b;
+    bool ok = len >= min_len;
+    for (int q = lane + 1; q < len && ok; q += 32) ok = idx[b + q] > idx[b + q - 1];
+    ok = __all_sync(0xffffffffu, ok);
+    int out = len;
+    if (ok) {
+        const long long span = (long long)idx[b + len - 1] - idx[b] + 1;
+        if (span - len <= len / 32) out = (int)span;
+    }
+    if (lane == 0) padlen[w] = out;
+}
+
+// copy rows into the padded layout: a padded row is pre-filled with
+// (column, 0.0, src -1) and its entries scattered to column - first column
+// (warp per row)
+__global__ void k_pad_gather(const int* ptr, const int* idx, const double* val, const int* src,
+                             int rows, const int* nptr, int* nidx, double* nval, int* nsrc) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const int b = ptr[w], len = ptr[w + 1] - b, d = nptr[w], nlen = nptr[w + 1] - d;
+    if (nlen == len) {
+        for (int q = lane; q < len; q += 32) {
+            nidx[d + q] = idx[b + q];
+            nval[d + q] = val[b + q];
+            nsrc[d + q] = src[b + q];
+        }
+        return;
+    }
+    const int j0 = idx[b];
+    for (int q = lane; q < nlen; q += 32) {
+        nidx[d + q] = j0 + q;
+        nval[d + q] = 0.0;
+        nsrc[d + q] = -1;
+    }
+    __syncwarp();
+    for (int q = lane; q < len; q += 32) {
+        const int p = d + (idx[b + q] - j0);
+        nval[p] = val[b + q];
+        nsrc[p] = src[b + q];
+    }
+}
+
+// rbase[i] = ptr[i] - idx[ptr[i]] when row i's columns are consecutive and
+// the row has >= min_len entries, else INT_MIN (warp per row)
+__global__ void k_dense_rows(const int* ptr, const int* idx, int rows, int min_len, int* rbase) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const int b = ptr[w], len = ptr[w + 1] - b;
+    bool ok = len >= min_len;
+    for (int q = lane + 1; q < len && ok; q += 32) ok = idx[b + q] == idx[b + q - 1] + 1;
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane == 0) rbase[w] = ok ? b - idx[b] : INT_MIN;
+}
+
+// Per F^T row j: the longest run of entries on consecutive dense F rows.
+// pinfo[j] = {i0, L} (L >= min_run, else {0, 0}), roff[j] = the run's first
+// entry within the row, keep[j] = entries left in F^T (a panel row keeps at
+// most max_keep, so its panel tile stages them); covered[0] += L,
+// covered[1] += 1 per panel column (thread per row).
+__global__ void k_col_panels(const int* ptr, const int* idx, int cols, const int* rbase,
+                             int min_run, int max_keep, int2* pinfo, int* roff, int* keep,
+                             unsigned long long* covered) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    const int b = ptr[j], len = ptr[j + 1] - b;
+    int best = 0, best_q = 0, cur = 0;
+    for (int q = 0; q < len; ++q) {
+        const int i = idx[b + q];
+        if (rbase[i] == INT_MIN) {
+            cur = 0;
+            continue;
+        }
+        if (cur > 0 && i == idx[b + q - 1] + 1) {
+            ++cur;
+        } else {
+            cur = 1;
+        }
+        if (cur > best) {
+            best = cur;
+            best_q = q - cur + 1;
+        }
+    }
+    if (best >= min_run && len - best <= max_keep) {
+        pinfo[j] = make_int2(idx[b + best_q], best);
+        roff[j] = best_q;
+        keep[j] = len - best;
+        atomicAdd(covered, (unsigned long long)best);
+        atomicAdd(covered + 1, 1ULL);
+    } else {
+        pinfo[j] = make_int2(0, 0);
+        roff[j] = 0;
+        keep[j] = len;
+    }
+}
+
+// F^T without its panel entries (thread per row, order kept)
+__global__ void k_drop_panels(const int* ptr, const int* idx, const double* val, const int* src,
+                              int cols, const int2* pinfo, const int* roff, const int* nptr,
+                              int* nidx, double* nval, int* nsrc) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    const int b = ptr[j], len = ptr[j + 1] - b;
+    const int r0 = roff[j], r1 = r0 + pinfo[j].y;
+    int d = nptr[j];
+    for (int q = 0; q < len; ++q) {
+        if (q >= r0 && q < r1) continue;
+        nidx[d] = idx[b + q];
+        nval[d] = val[b + q];
+        nsrc[d] = src[b + q];
+        ++d;
+    }
 }
 
 // input checks: indptr monotone and in range, columns in range

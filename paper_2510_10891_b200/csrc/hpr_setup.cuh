@@ -427,7 +427,7 @@ __global__ void k_restart_copy(const Ctrl* c, int n, int m, int nf, const double
 __global__ void k_gather_vals(double* dst, const double* src, const int* map, long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        dst[i] = src[map[i]];
+        dst[i] = map[i] >= 0 ? src[map[i]] : 0.0;   // < 0: explicit zero (padded flow row)
 }
 
 // caller order <-> engine order (locality permutation)

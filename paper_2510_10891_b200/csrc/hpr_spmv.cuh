@@ -67,7 +67,7 @@ __device__ __forceinline__ void block_store(Acc<K>& acc, double* part, int nslot
 }
 
 template <typename T, class Epi>
-__global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
+__global__ void __launch_bounds__(TPB, 16) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
     __shared__ T prod[TILE_NNZ];
     __shared__ int sptr[TILE_ROWS + 1];
     __shared__ T wpart[TPB / 32];
@@ -75,7 +75,67 @@ __global__ void __launch_bounds__(TPB) k_spmv(Csr<T> A, const T* __restrict__ xg
     Acc<Epi::K> acc;
     acc.zero();
     const int4 tl = A.tiles[blockIdx.x];
-    if (tl.y < 0) {
+    if (tl.y < 0 && tl.w < 0) {
+        // ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= 32 rows with flow panels -------
+        // Remaining (indexed) entries are staged as in a stream tile; the dense
+        // part is read from F's row-major values: lane = row, warp = every 4th
+        // panel row, so each load of a warp is one contiguous 256-byte segment
+        // of a flow row and y is a warp-uniform broadcast.
+        __shared__ T ppart[TPB / 32][PANEL_ROWS];
+        const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = -tl.w - 1 - tl.z;
+        const int R = r1 - r0;
+        {
+            const int* __restrict__ idx = A.indices + p0;
+            const T* __restrict__ val = A.vals + p0;
+            for (int e = threadIdx.x; e < cnt; e += TPB) prod[e] = ld_stream(val + e) * ld_ro(xg + ld_stream(idx + e));
+            if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
+            if (threadIdx.x == 0) sptr[R] = cnt;
+        }
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int4 pd = A.pdesc[blockIdx.x];
+        T s = T(0);
+        if (lane < R) {
+            const int r = r0 + lane;
+            if (pd.w > 0) {
+                // one row-major block: no per-row lookups between the tile and the loads
+                const T* __restrict__ pv = A.pvals + ((long long)pd.z + r);
+                const T* __restrict__ yv = xg + pd.x;
+                constexpr int U = 4;
+                int q = warp;
+                for (; q + (U - 1) * (TPB / 32) < pd.y; q += U * (TPB / 32)) {
+                    T v[U], g[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int qq = q + u * (TPB / 32);
+                        v[u] = ld_stream(pv + (long long)qq * pd.w);
+                        g[u] = ld_ro(yv + qq);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) s += v[u] * g[u];
+                }
+                for (; q < pd.y; q += TPB / 32) s += ld_stream(pv + (long long)q * pd.w) * ld_ro(yv + q);
+            } else {
+                const int2 pi = A.pinfo[r];
+#pragma unroll 4
+                for (int q = warp; q < pi.y; q += TPB / 32) {
+                    const int i = pi.x + q;
+                    s += ld_stream(A.pvals + ((long long)__ldg(A.rbase + i) + r)) * ld_ro(xg + i);
+                }
+            }
+        }
+        ppart[warp][lane] = s;
+        __syncthreads();
+        if (threadIdx.x < R) {
+            const int k = threadIdx.x;
+            T t = T(0);
+            for (int q = sptr[k]; q < sptr[k + 1]; ++q) t += prod[q];
+            T pv = ppart[0][k];
+#pragma unroll
+            for (int w = 1; w < TPB / 32; ++w) pv += ppart[w][k];
+            epi.apply(r0 + k, t + pv, acc);
+        }
+        block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
+    } else if (tl.y < 0) {
         // ---------------- stream tile {r0, -(r1+1), p0, p1} ----------------
         const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = tl.w - tl.z;
         const int R = r1 - r0;

@@ -208,7 +208,7 @@ class Engine:
     the engine's kernels run on a private CUDA stream of the handle."""
 
     def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True,
-                 runs: bool = True, comm=None):
+                 runs: bool = True, panels: bool = True, comm=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("the HPR engine needs a CUDA device (no CPU fallback)")
@@ -236,7 +236,8 @@ class Engine:
         self._ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=f"cuda:{dev}")
         flags = ((0 if reorder else _capi.HPR_FLAG_NO_REORDER)
                  | (0 if fold else _capi.HPR_FLAG_NO_FOLD)
-                 | (0 if runs else _capi.HPR_FLAG_NO_RUNS))
+                 | (0 if runs else _capi.HPR_FLAG_NO_RUNS)
+                 | (0 if panels else _capi.HPR_FLAG_NO_PANELS))
         ncomm, world, rank = (None, 1, 0) if comm is None else (comm.handle, comm.world_size,
                                                                  comm.rank)
         opt = _capi.Options(dev, None, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
@@ -317,8 +318,9 @@ class Engine:
         return {k: getattr(lay, k) for k, _ in lay._fields_}
 
     def bench_kernel(self, which: int, reps: int = 20) -> float:
-        """Average device seconds of one fused iteration kernel
-        (0: A x~ + dual update, 1: A^T y + primal update)."""
+        """Average device seconds of one iteration kernel (hpr_bench_kernel:
+        0: A x~ product, 1: A^T y product, 2: primal update, 3: dual update,
+        4: one KKT check block)."""
         sec = _capi.C.c_double()
         _capi.check(self._lib.hpr_bench_kernel(self._h, int(which), int(reps),
                                                _capi.C.byref(sec)))

@@ -69,3 +69,13 @@ def test_direct_ptdf_rows_match_reference_tables():
         rows = scuc._ptdf_rows_direct(inst.B, inst.net.fb, inst.net.tb, inst.net.react,
                                       inst.net.ref, lines, skip=skip)
         np.testing.assert_allclose(rows, ref.table(key)[lines], rtol=0, atol=1e-12)
+
+
+def test_c1_digest_matches_golden_fixture():
+    """The C1 LP this builder makes is the one the reference trajectory
+    fixture (tests/golden/c1_trajectory.json) was recorded on."""
+    from tests import golden_io
+    g = golden_io.c1()
+    doc, mon, lp = scuc.build_config("C1")
+    assert lp.shape == tuple(g["shape"]) and lp.nnz == g["nnz"]
+    assert lp.digest() == g["digest"]

@@ -1,0 +1,108 @@
+"""Drop-in check: the reference's successive fixing (scuckit.fixing, Alg. 2)
+with its LP solves routed to the B200 engine by ``hprlp.install()``.
+
+Needs the reference package importable: the build container's
+/root/reference, or the ``baseline/_ref`` install that travels to the GPU
+box (``pip install --no-deps --target baseline/_ref <reference pkg>``).  The
+north-star criterion: identical fixed-variable sets wherever no relaxed
+binary lies within 1e-6 of a fixing threshold, and LP objectives within the
+solver tolerance.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _scuckit():
+    for p in (REF, "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "scuckit")) and p not in sys.path:
+            sys.path.append(p)
+    try:
+        import scuckit  # noqa: F401
+        return True
+    except Exception:
+        return False
+
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not _scuckit(), reason="reference package not installed")]
+
+
+def _fixing_run(doc, rounds=2, tau=0.1):
+    from scuckit import (apply_instance_scaling, build_model, hprlp, lp_backends,
+                         parse_instance, successive_fixing)
+    from paper_2510_10891_b200 import scuc
+    inst, _ = apply_instance_scaling(parse_instance(doc))
+    model, _ = build_model(inst, monitored=scuc.all_base_triples(doc))
+    cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False)
+    rec = []
+
+    def solver(lp):
+        r = lp_backends.solve_lp(lp, "hpr", cfg)
+        rec.append((r.objective, r.iterations, r.status, r.x))
+        return r
+
+    error = None
+    try:
+        successive_fixing(model, rounds, solver, tau)    # fixes accumulate on `model`
+    except Exception as exc:                              # e.g. InfeasibleModelError
+        error = f"{type(exc).__name__}: {exc}"
+    return rec, {k: v.value for k, v in model.fixed.items()}, error
+
+
+def _near_threshold(x, tau, tol=1e-6):
+    x = np.asarray(x)
+    return bool(np.any((np.abs(x - tau) < tol) | (np.abs(x - (1 - tau)) < tol)))
+
+
+def test_successive_fixing_gpu_matches_cpu():
+    """Small instance: the reference loop twice on the box, CPU HPR vs GPU."""
+    import scuckit.hprlp as ref_hprlp
+    from paper_2510_10891_b200 import hprlp as gpu, scuc
+    doc = scuc.generate_instance(30, 12, 45, 8, seed=3)
+    cpu_rec, cpu_fixed, cpu_err = _fixing_run(doc)
+    gpu.install()
+    try:
+        assert ref_hprlp.solve is gpu.solve
+        gpu_rec, gpu_fixed, gpu_err = _fixing_run(doc)
+    finally:
+        gpu.uninstall()
+    assert ref_hprlp.solve is not gpu.solve
+    assert len(gpu_rec) == len(cpu_rec)
+    for (oc, ic, sc, xc), (og, ig, sg, xg) in zip(cpu_rec, gpu_rec):
+        assert sc == sg == "optimal-tolerance"
+        assert abs(og - oc) <= 1e-6 * abs(oc)
+    if not any(_near_threshold(r[3], 0.1) for r in cpu_rec):
+        assert gpu_fixed == cpu_fixed and gpu_err == cpu_err
+
+
+def test_successive_fixing_c1_against_reference_record():
+    """C1 structure (118 buses, 54 units, 24 periods, all base flow rows):
+    the GPU-driven fixing loop against the reference's own CPU record
+    (tests/golden/c1_fixing.json, produced by make_fixing_golden.py)."""
+    path = os.path.join(ROOT, "tests", "golden", "c1_fixing.json")
+    if not os.path.exists(path):
+        pytest.skip("c1_fixing.json not generated")
+    g = json.load(open(path))
+    import scuckit.hprlp as ref_hprlp
+    from paper_2510_10891_b200 import hprlp as gpu, scuc
+    doc = scuc.generate_instance(**scuc.CONFIGS["C1"])
+    gpu.install()
+    try:
+        rec, fixed, err = _fixing_run(doc)
+    finally:
+        gpu.uninstall()
+    assert len(rec) == len(g["rounds"])
+    for (og, ig, sg, xg), r in zip(rec, g["rounds"]):
+        assert sg == r["status"]
+        assert abs(og - r["objective"]) <= 1e-6 * abs(r["objective"])
+    want = {int(k): v for k, v in g["fixed"].items()}
+    if not any(_near_threshold(r[3], 0.1) for r in rec):
+        assert fixed == want and err == g["error"]

@@ -240,25 +240,70 @@ def test_twin_folding_is_transparent(H):
     np.testing.assert_allclose(a, b, rtol=1e-8, atol=1e-14)
 
 
-def test_run_compressed_chunks_bit_identical(H):
-    """Dense PTDF flow rows (> 2048 nonzeros) are streamed without their index
-    array; the products must be bit-identical to the indexed path."""
+def test_flow_panels_are_transparent(H):
+    """A^T y's dense flow block read from F's row-major values (panels) instead
+    of F^T: same solve up to FP64 reassociation noise, same KKT evaluation,
+    and the layout drops exactly the panel entries from F^T."""
+    from paper_2510_10891_b200 import scuc
+    from oracle import hpr_oracle as Ora
+    doc, mon, lpa = scuc.build_config("C3", n_triples=600)     # ~17 flow rows per period
+    lp = lpa.to_lp()
+    cfg = H.SolverConfig(tolerance=1e-8, ruiz=False, max_iterations=480, log_residuals=True)
+    res, kk = {}, {}
+    rng = np.random.default_rng(11)
+    pt = (rng.standard_normal(lpa.shape[1]), np.abs(rng.standard_normal(lpa.shape[0])),
+          rng.standard_normal(lpa.shape[1]))
+    for panels in (False, True):
+        eng = H.Engine(lp, panels=panels)
+        lay = eng.layout()
+        if panels:
+            assert lay["panel_nnz"] > 0.5 * lay["folded_nnz"] and lay["panel_cols"] > 0
+            assert lay["ft_nnz"] == lay["folded_nnz"] - lay["panel_nnz"]
+        else:
+            assert lay["panel_nnz"] == 0 and lay["ft_nnz"] == lay["folded_nnz"]
+        res[panels] = eng.solve_raw(cfg)
+        kk[panels] = eng.kkt(*pt)
+        eng.close()
+    (x0, y0, z0, s0, l0), (x1, y1, z1, s1, l1) = res[False], res[True]
+    assert s0.lam == s1.lam and s0.iterations == s1.iterations == 480
+    a = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in l0])
+    b = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in l1])
+    np.testing.assert_allclose(a[:12], b[:12], rtol=1e-8, atol=1e-14)
+    np.testing.assert_allclose(x1, x0, rtol=1e-6, atol=1e-8)
+    for f in ("primal", "dual", "box", "rel_gap"):
+        assert getattr(kk[True], f) == pytest.approx(getattr(kk[False], f), rel=1e-11)
+    # and against the oracle's KKT of the same point (FP64 master data)
+    ko = Ora.kkt(Ora.Problem.from_lp(lp), *pt)
+    assert kk[True].dual == pytest.approx(ko.dual, rel=1e-10)
+
+
+def test_index_free_flow_rows(H):
+    """Dense PTDF flow rows are padded with explicit zeros to single column
+    runs and streamed without their index array.  The padding only moves the
+    summation's association: the products are the same, the solve agrees to
+    FP64 reassociation noise, and A x (unpadded operand) is bit-identical."""
     from paper_2510_10891_b200 import scuc
     doc, mon, lpa = scuc.build_config("C3", n_triples=60)
     lp = lpa.to_lp()
-    cfg = H.SolverConfig(tolerance=1e-8, ruiz=False, max_iterations=320)
+    cfg = H.SolverConfig(tolerance=1e-8, ruiz=False, max_iterations=320, log_residuals=True)
     out = {}
     for runs in (False, True):
         eng = H.Engine(lp, runs=runs)
+        lay = eng.layout()
+        assert (lay["index_free_nnz_f"] > 0) == runs
+        assert (lay["f_nnz"] > lay["folded_nnz"]) == runs            # explicit zeros
         rng = np.random.default_rng(3)
         v = rng.standard_normal(lpa.shape[1])
         out[runs] = (eng.solve_raw(cfg), eng.matvec(v))
         eng.close()
     (a, ma), (b, mb) = out[False], out[True]
     assert np.array_equal(ma, mb)
-    for k in range(3):
-        assert np.array_equal(a[k], b[k])
     assert a[3].iterations == b[3].iterations == 320
+    la = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in a[4]])
+    lb = np.array([[r.rel_primal, r.rel_dual, r.rel_gap] for r in b[4]])
+    np.testing.assert_allclose(la, lb, rtol=1e-8, atol=1e-14)
+    for k in range(3):
+        np.testing.assert_allclose(a[k], b[k], rtol=1e-7, atol=1e-9)
 
 
 def test_c1_against_reference_trajectory(H):
@@ -330,3 +375,58 @@ def test_partitioned_engine_single_rank(H):
     assert abs(r.objective - ref.objective) <= 1e-7 * abs(ref.objective)
     assert O.kkt(O.Problem.from_lp(lpa), r.x, r.y, r.z).max_rel <= 1e-5 * 1.000001
     assert r_tl.status.value == "time-limit"
+
+
+def _edge_lp(kind, seed=5):
+    rng = np.random.default_rng(seed)
+    n, m = 18, 12
+    a = rng.standard_normal((m, n)) * (rng.uniform(size=(m, n)) < 0.5)
+    a[np.arange(m), rng.integers(0, n, m)] += 1.0
+    xf = rng.uniform(-0.5, 0.5, n)
+    lower, upper = -np.ones(n) * 2, np.ones(n) * 2
+    rhs = a @ xf
+    n_eq = m if kind == "all_eq" else 3
+    if kind == "empty_row":
+        a[5] = 0.0                        # 0 >= rhs_5 (<= 0) holds
+        rhs[5] = -1.0
+    if kind == "empty_col":
+        a[:, 7] = 0.0
+    if kind == "inf_bounds":
+        upper[::3] = np.inf
+        lower[1::4] = -np.inf
+        cost_sign = np.where(~np.isfinite(upper), 1.0, np.where(~np.isfinite(lower), -1.0, 0.0))
+    rhs[n_eq:] -= rng.uniform(0, 1, m - n_eq) * (kind != "empty_row")
+    y = rng.standard_normal(m)
+    y[n_eq:] = np.abs(y[n_eq:])
+    z = rng.standard_normal(n)
+    if kind == "inf_bounds":
+        z = np.where(cost_sign != 0, cost_sign * np.abs(z), z)
+    import scipy.sparse as sp
+    A = sp.csr_matrix(a)
+    A.eliminate_zeros()
+    return golden_io.FixtureLp(A.indptr, A.indices, A.data, A.shape, rhs, a.T @ y + z, lower,
+                               upper, n_eq)
+
+
+@pytest.mark.parametrize("kind", ["all_eq", "empty_row", "empty_col", "inf_bounds"])
+def test_edge_lps_vs_oracle(H, kind):
+    lp = _edge_lp(kind)
+    for cfg in (dict(tolerance=1e-7), dict(tolerance=1e-7, ruiz=False, log_residuals=True)):
+        ref = O.solve(lp, O.OracleConfig(**cfg))
+        r = H.solve(lp, H.SolverConfig(**cfg))
+        assert r.status.value == ref.status
+        assert r.lam == pytest.approx(ref.lam, rel=1e-12)
+        assert abs(r.objective - ref.objective) <= 1e-6 * max(1.0, abs(ref.objective))
+        assert abs(r.iterations - ref.iterations) <= max(32, 0.05 * ref.iterations)
+
+
+def test_two_engines_concurrently(H):
+    """Distinct handles are independent."""
+    lps = [golden_io.random_lps()[i][0] for i in (4, 9)]
+    engs = [H.Engine(lp) for lp in lps]
+    outs = [e.solve_raw(H.SolverConfig(tolerance=1e-8)) for e in engs]
+    for lp, o in zip(lps, outs):
+        ref = O.solve(lp, O.OracleConfig(tolerance=1e-8))
+        assert abs(float(np.dot(lp.cost, o[0])) - ref.objective) <= 1e-6 * max(1, abs(ref.objective))
+    for e in engs:
+        e.close()
