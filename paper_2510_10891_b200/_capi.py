@@ -28,7 +28,9 @@ EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_crea
            "hpr_destroy", "hpr_solve", "hpr_get_log", "hpr_matvec", "hpr_kkt_residual",
            "hpr_power_method", "hpr_iterate", "hpr_resume", "hpr_bench_kernel",
            "hpr_get_layout", "hpr_nccl_unique_id", "hpr_nccl_comm_init",
-           "hpr_nccl_comm_destroy")
+           "hpr_nccl_comm_destroy",
+           # include/hpr_presolve.h (host-only presolve core)
+           "hpr_presolve_run", "hpr_presolve_info", "hpr_presolve_fetch", "hpr_presolve_free")
 
 _p = C.c_void_p
 
@@ -133,6 +135,11 @@ def load(path: str | None = None):
                                        C.POINTER(_p)]
     lib.hpr_nccl_comm_destroy.argtypes = [_p]
     lib.hpr_nccl_comm_destroy.restype = None
+    lib.hpr_presolve_run.argtypes = [_p, C.c_int32, C.POINTER(_p)]
+    lib.hpr_presolve_info.argtypes = [_p, _p]
+    lib.hpr_presolve_fetch.argtypes = [_p] * 8
+    lib.hpr_presolve_free.argtypes = [_p]
+    lib.hpr_presolve_free.restype = None
     _LIB = lib
     return lib
 

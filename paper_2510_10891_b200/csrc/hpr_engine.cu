@@ -855,6 +855,34 @@ void read_ctrl(hpr_handle* h) {
     CK(cudaStreamSynchronize(h->stream));
 }
 
+// HPR_EAGER=1 (or HPR_SYNC_DEBUG): the block loop as plain stream launches
+// with a host status read per block — for profilers that cannot look inside
+// conditional graph nodes (ncu); no wall-clock deadline.  Returns device seconds.
+static bool eager_loop() {
+    static const bool on = getenv("HPR_EAGER") != nullptr;
+    return on || sync_debug();
+}
+
+template <typename T>
+double run_eager(hpr_handle* h, int B) {
+    cudaStream_t s = h->stream;
+    const Ptrs<T> p = ptrs<T>(h);
+    unsigned long long zero = 0;
+    CK(cudaMemcpyAsync(&h->ctrl->cond, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+    float total = 0.f;
+    do {
+        CK(cudaEventRecord(h->ev[2], s));
+        for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, s);
+        enqueue_check<T>(h, p, 1, s);
+        CK(cudaEventRecord(h->ev[3], s));
+        read_ctrl(h);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+        total += ms;
+    } while (h->h_ctrl->status == -1);
+    return total * 1e-3;
+}
+
 void cast_work_vectors(hpr_handle* h) {
     cudaStream_t s = h->stream;
     const int m = h->m, n = h->n;
@@ -973,16 +1001,8 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
                 CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
             }
         }
-        if (sync_debug() && !h->comm) {
-            // eager block loop (no graph, no deadline): debugging only
-            const auto t0 = std::chrono::steady_clock::now();
-            do {
-                for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, s);
-                enqueue_check<T>(h, p, 1, s);
-                read_ctrl(h);
-            } while (h->h_ctrl->status == -1);
-            st->loop_seconds =
-                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (eager_loop() && !h->comm) {
+            st->loop_seconds = run_eager<T>(h, B);
         } else {
             ensure_graph<T>(h, p, B);
             st->loop_seconds = run_loop(h, time_left);
@@ -1728,7 +1748,8 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
 int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* st) {
     API_BEGIN
     if (!h || !st) fail(HPR_ERR_INVALID, "NULL argument");
-    if (h->last_prec < 0 || !h->gexec) fail(HPR_ERR_INVALID, "hpr_resume needs a prior looping solve");
+    if (h->last_prec < 0 || (!h->gexec && !eager_loop()))
+        fail(HPR_ERR_INVALID, "hpr_resume needs a prior looping solve");
     CK(cudaSetDevice(h->dev));
     std::memset(st, 0, sizeof(*st));
     h->launches = 0;
@@ -1741,7 +1762,11 @@ int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_sta
     c.cond = 0;
     CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     *h->h_ctrl = c;
-    st->loop_seconds = c.status == -1 ? run_loop(h) : 0.0;
+    if (c.status != -1) st->loop_seconds = 0.0;
+    else if (eager_loop() && !h->comm)
+        st->loop_seconds = h->last_prec == HPR_FP32 ? run_eager<float>(h, (int)c.B)
+                                                    : run_eager<double>(h, (int)c.B);
+    else st->loop_seconds = run_loop(h);
     const Ctrl& hc = *h->h_ctrl;
     st->status = hc.status;
     st->precision_used = h->last_prec;

@@ -609,17 +609,25 @@ def solve_partitioned(lp, config=None, start=None, comm: NcclComm | None = None,
 _SAVED = {}
 
 
-def install(module=None):
+_PRESOLVE_SITES = ("scuckit.presolve", "scuckit.fixing", "scuckit.milp_bb", "scuckit")
+
+
+def install(module=None, presolve: bool = True):
     """Route the reference's LP solves to the GPU engine.
 
     Rebinds ``scuckit.hprlp.solve`` (and ``kkt_residual`` / ``hpr_iterate``)
-    and switches result construction to the reference's own classes."""
+    and switches result construction to the reference's own classes.  With
+    ``presolve`` the reference's ``milp_presolve`` / ``lp_presolve`` are
+    rebound too, in every module that imported them by name (presolve.py,
+    fixing.py:22, milp_bb.py:26, the package namespace), to the native-core
+    mirror in ``paper_2510_10891_b200.presolve`` (bit-identical reductions)."""
+    import importlib
     if module is None:
         import scuckit.hprlp as module
     from scuckit import lp_kernel
     if "solve" not in _SAVED:
         _SAVED.update(solve=module.solve, kkt_residual=module.kkt_residual,
-                      hpr_iterate=module.hpr_iterate, module=module)
+                      hpr_iterate=module.hpr_iterate, module=module, presolve={})
     _CLS.status = module.SolveStatus
     _CLS.result = module.SolveResult
     _CLS.kkt = module.KktResidual
@@ -627,16 +635,31 @@ def install(module=None):
     module.solve = solve
     module.kkt_residual = kkt_residual
     module.hpr_iterate = hpr_iterate
+    if presolve:
+        from . import presolve as native
+        ref = importlib.import_module("scuckit.presolve")
+        native._LOG_CLASS = ref.ReductionLog
+        for name in _PRESOLVE_SITES:
+            mod = importlib.import_module(name)
+            for fn in ("milp_presolve", "lp_presolve"):
+                if hasattr(mod, fn):
+                    _SAVED["presolve"].setdefault((name, fn), getattr(mod, fn))
+                    setattr(mod, fn, getattr(native, fn))
     return module
 
 
 def uninstall():
     if not _SAVED:
         return
+    import importlib
     module = _SAVED["module"]
     module.solve = _SAVED["solve"]
     module.kkt_residual = _SAVED["kkt_residual"]
     module.hpr_iterate = _SAVED["hpr_iterate"]
+    for (name, fn), orig in _SAVED.get("presolve", {}).items():
+        setattr(importlib.import_module(name), fn, orig)
+    from . import presolve as native
+    native._LOG_CLASS = native.ReductionLog
     _CLS.status, _CLS.result, _CLS.kkt, _CLS.precision = (SolveStatus, SolveResult,
                                                           KktResidual, Precision)
     _SAVED.clear()

@@ -86,3 +86,28 @@ class StandardFormLp:
     def objective(self, x: np.ndarray) -> float:
         return float(np.dot(np.asarray(self.cost, np.float64),
                             np.asarray(x, np.float64))) + self.offset
+
+
+class MilpModel:
+    """Mirror of ``formulation.MilpModel`` (``formulation.py:100-145``): the
+    LP plus integrality marks (what presolve reads and returns)."""
+
+    def __init__(self, lp: StandardFormLp, integrality, vmap=None):
+        self.lp = lp
+        self.integrality = np.asarray(integrality, dtype=bool)
+        self.vmap = vmap
+        self.fixed: dict = {}
+
+    @property
+    def n_rows(self) -> int:
+        return self.lp.n_rows
+
+    @property
+    def n_cols(self) -> int:
+        return self.lp.n_cols
+
+    def relax(self) -> StandardFormLp:
+        lp = self.lp
+        return StandardFormLp(lp.matrix, lp.rhs.copy(), lp.cost.copy(), lp.lower.copy(),
+                              lp.upper.copy(), lp.n_eq, lp.offset, list(lp.row_tags),
+                              list(lp.col_tags))

@@ -1,0 +1,226 @@
+"""Drop-in mirror of ``scuckit.presolve`` (pkg/src/scuckit/presolve.py) whose
+row-queue fixpoint runs in the native core (include/hpr_presolve.h,
+csrc/hpr_presolve.cpp).
+
+``milp_presolve`` / ``lp_presolve`` take and return the caller's own model
+classes (the reference's ``MilpModel`` / ``StandardFormLp`` / ``SparseMatrix``
+when called from the reference's fixing loop or B&B, this package's mirrors
+otherwise) and assemble the reduced model with the same numpy / scipy
+operations as presolve.py:212-288, so the reduced model, the reduction log and
+the infeasibility messages are identical to the reference's.
+``hprlp.install()`` rebinds them into ``scuckit.presolve``, ``scuckit.fixing``
+and ``scuckit.milp_bb``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+
+_FIXED_TOL = 1e-10        # presolve.py:24
+_MAX_PASSES = 100         # presolve.py:195
+
+
+class InfeasibleModelError(RuntimeError):
+    """Mirror of presolve.py:27-29 (raised by callers, never by presolve)."""
+
+
+@dataclass
+class ReductionLog:
+    """Mirror of ``ReductionLog`` (presolve.py:32-48)."""
+
+    n_cols_full: int
+    n_rows_full: int
+    kept_cols: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=np.int64))
+    kept_rows: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=np.int64))
+    fixed_values: dict = field(default_factory=dict)
+    removed_rows: list = field(default_factory=list)
+    bound_changes: list = field(default_factory=list)
+    objective_delta: float = 0.0
+    infeasible: str | None = None
+
+    @property
+    def feasible(self) -> bool:
+        return self.infeasible is None
+
+
+# the log class handed back to callers; install() points it at the reference's
+_LOG_CLASS = ReductionLog
+
+
+def uncrush(point: np.ndarray, log) -> np.ndarray:
+    """Lift a reduced-space point to the full column space (presolve.py:51-62)."""
+    point = np.asarray(point, dtype=np.float64)
+    if point.shape[0] != log.kept_cols.shape[0]:
+        raise ValueError(f"point has {point.shape[0]} entries; log expects "
+                         f"{log.kept_cols.shape[0]}")
+    full = np.zeros(log.n_cols_full)
+    full[log.kept_cols] = point
+    for col, val in log.fixed_values.items():
+        full[col] = val
+    return full
+
+
+class _Problem(C.Structure):
+    _fields_ = [("m", C.c_int32), ("n", C.c_int32), ("n_eq", C.c_int32),
+                ("indptr", C.c_void_p), ("indices", C.c_void_p), ("data", C.c_void_p),
+                ("col_ptr", C.c_void_p), ("col_rows", C.c_void_p), ("rhs", C.c_void_p),
+                ("lower", C.c_void_p), ("upper", C.c_void_p), ("integrality", C.c_void_p)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("status", C.c_int32), ("index", C.c_int32), ("v1", C.c_double),
+                ("v2", C.c_double), ("n_changes", C.c_int64), ("n_removed", C.c_int64),
+                ("visits", C.c_int64)]
+
+
+_REASONS = ("empty", "redundant")
+
+
+class _Reduction:
+    """Result of one native fixpoint run over an LP (the state _Reducer holds
+    after ``run()``, presolve.py:65-209)."""
+
+    def __init__(self, lp, integrality):
+        lib = _capi.load()
+        self.csr = lp.matrix.csr.astype(np.float64)
+        csc = lp.matrix.csc
+        self.rhs = lp.rhs.astype(np.float64).copy()
+        self.cost = lp.cost.astype(np.float64)
+        lower = np.ascontiguousarray(lp.lower, dtype=np.float64)
+        upper = np.ascontiguousarray(lp.upper, dtype=np.float64)
+        self.n_eq = int(lp.n_eq)
+        self.m, self.n = self.csr.shape
+        self.row_tags = lp.row_tags or [f"row {i}" for i in range(self.m)]
+        self.col_tags = lp.col_tags or [f"col {j}" for j in range(self.n)]
+        keep = [np.ascontiguousarray(self.csr.indptr, dtype=np.int64),
+                np.ascontiguousarray(self.csr.indices, dtype=np.int32),
+                np.ascontiguousarray(self.csr.data, dtype=np.float64),
+                np.ascontiguousarray(csc.indptr, dtype=np.int64),
+                np.ascontiguousarray(csc.indices, dtype=np.int32),
+                np.ascontiguousarray(self.rhs), lower, upper]
+        integ = None
+        if integrality is not None:
+            integ = np.ascontiguousarray(np.asarray(integrality, dtype=bool), dtype=np.uint8)
+            keep.append(integ)
+        def addr(a):
+            return a.ctypes.data if (a is not None and a.size) else None
+
+        def ptr(a):
+            return C.c_void_p(addr(a))
+
+        prob = _Problem(self.m, self.n, self.n_eq, *[addr(a) for a in keep[:8]], addr(integ))
+        h = C.c_void_p()
+        if lib.hpr_presolve_run(C.addressof(prob), _MAX_PASSES, C.byref(h)) != 0:
+            raise ValueError("hpr_presolve_run rejected the model")
+        try:
+            info = _Info()
+            lib.hpr_presolve_info(h, C.addressof(info))
+            nc, nr = int(info.n_changes), int(info.n_removed)
+            self.alive_row = np.empty(self.m, dtype=np.uint8)
+            self.lower = np.empty(self.n)
+            self.upper = np.empty(self.n)
+            ccol = np.empty(nc, dtype=np.int32)
+            cb = np.empty(4 * nc)
+            rrow = np.empty(nr, dtype=np.int32)
+            rwhy = np.empty(nr, dtype=np.int8)
+            lib.hpr_presolve_fetch(h, ptr(self.alive_row), ptr(self.lower), ptr(self.upper),
+                                   ptr(ccol), ptr(cb), ptr(rrow), ptr(rwhy))
+        finally:
+            lib.hpr_presolve_free(h)
+        self.alive_row = self.alive_row.astype(bool)
+        cb = cb.reshape(nc, 4)
+        self.changes = [(int(j), float(a), float(b), float(c), float(d))
+                        for j, (a, b, c, d) in zip(ccol.tolist(), cb.tolist())]
+        self.removed = [(int(i), _REASONS[w]) for i, w in zip(rrow.tolist(), rwhy.tolist())]
+        self.visits = int(info.visits)
+        self.infeasible = self._certificate(info)
+
+    def _certificate(self, info):
+        """The reference's infeasibility message (presolve.py:116-118, 133-148)."""
+        i, s = int(info.index), int(info.status)
+        if s == 0:
+            return None
+        if s == 1:
+            return f"row {i} ({self.row_tags[i]}) is empty with rhs {self.rhs[i]}"
+        if s == 2:
+            return (f"row {i} ({self.row_tags[i]}): max activity {float(info.v1)} "
+                    f"cannot reach rhs {self.rhs[i]}")
+        if s == 3:
+            return (f"row {i} ({self.row_tags[i]}): min activity {float(info.v1)} "
+                    f"exceeds rhs {self.rhs[i]}")
+        return (f"column {i} ({self.col_tags[i]}) has empty domain "
+                f"[{np.float64(info.v1)}, {np.float64(info.v2)}]")
+
+
+def _new_log(lp, red):
+    log = _LOG_CLASS(n_cols_full=lp.n_cols, n_rows_full=lp.n_rows)
+    log.bound_changes = red.changes
+    log.removed_rows = red.removed
+    return log
+
+
+def milp_presolve(model):
+    """Reduce a MILP (presolve.py:212-257): fixed-column substitution, bound
+    tightening with integral rounding, redundant-row removal.  Returns the
+    reduced model (the caller's classes) and the reduction log."""
+    lp = model.lp
+    red = _Reduction(lp, model.integrality)
+    log = _new_log(lp, red)
+    if red.infeasible:
+        log.infeasible = red.infeasible
+        log.kept_cols = np.arange(lp.n_cols, dtype=np.int64)
+        log.kept_rows = np.arange(lp.n_rows, dtype=np.int64)
+        return model, log
+
+    fixed = (red.upper - red.lower) <= _FIXED_TOL
+    fixed_at = 0.5 * (red.upper + red.lower)
+    cols = np.flatnonzero(~fixed)
+    rows = np.flatnonzero(red.alive_row)
+    log.kept_cols = cols.astype(np.int64)
+    log.kept_rows = rows.astype(np.int64)
+    log.fixed_values = {int(j): float(fixed_at[j]) for j in np.flatnonzero(fixed)}
+    log.objective_delta = float(red.cost[fixed] @ fixed_at[fixed])
+    shift = (red.csr @ np.where(fixed, fixed_at, 0.0)) if fixed.any() else np.zeros(lp.n_rows)
+    reduced_lp = type(lp)(
+        matrix=type(lp.matrix)(red.csr[rows][:, cols]),
+        rhs=(red.rhs - shift)[rows],
+        cost=red.cost[cols].copy(),
+        lower=red.lower[cols],
+        upper=red.upper[cols],
+        n_eq=int(np.count_nonzero(rows < lp.n_eq)),
+        offset=lp.offset + log.objective_delta,
+        row_tags=[red.row_tags[i] for i in rows],
+        col_tags=[red.col_tags[j] for j in cols],
+    )
+    return type(model)(reduced_lp, model.integrality[cols], vmap=None), log
+
+
+def lp_presolve(lp):
+    """LP-only reduction (presolve.py:260-288): tightening, redundant rows and
+    singleton rows; columns are never removed."""
+    red = _Reduction(lp, None)
+    log = _new_log(lp, red)
+    log.kept_cols = np.arange(lp.n_cols, dtype=np.int64)
+    if red.infeasible:
+        log.infeasible = red.infeasible
+        log.kept_rows = np.arange(lp.n_rows, dtype=np.int64)
+        return lp, log
+    rows = np.flatnonzero(red.alive_row)
+    log.kept_rows = rows.astype(np.int64)
+    reduced = type(lp)(
+        matrix=type(lp.matrix)(red.csr[rows]),
+        rhs=red.rhs[rows],
+        cost=red.cost.copy(),
+        lower=red.lower,
+        upper=red.upper,
+        n_eq=int(np.count_nonzero(rows < lp.n_eq)),
+        offset=lp.offset,
+        row_tags=[red.row_tags[i] for i in rows],
+        col_tags=list(red.col_tags),
+    )
+    return reduced, log

@@ -1,5 +1,5 @@
 """The C-ABI library loads on a CPU-only host and exports every entry point
-declared in include/hprlp_b200.h (no compute calls here)."""
+declared in include/*.h (no compute calls here)."""
 
 import ctypes
 import os
@@ -11,7 +11,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def header_functions():
-    src = open(os.path.join(ROOT, "include", "hprlp_b200.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc))
+                  if f.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"^\s*(?:int|int32_t|void|const char\*)\s+\**(hpr_\w+)\s*\(",
                                  src, flags=re.M)))

@@ -1,0 +1,55 @@
+"""End-to-end successive-fixing wall time (north star "reported results"):
+the reference's own transmission-filtered two-stage driver (scuckit.driver.run,
+driver.py:203-325) on a synthetic instance, with its LP relaxations either on
+the reference CPU HPR solver (--backend cpu) or routed to the B200 engine by
+hprlp.install() (--backend gpu; nothing else in the driver changes).
+
+Needs the reference package: baseline/_ref (travels to the GPU box) or
+/root/reference/pkg/src.  Prints one JSON line with the driver's RunReport
+timings (lp_relaxations / other / total), status, objective and passes.
+
+    python tools/sf_e2e.py --backend gpu --config C1 --time-limit 1500
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(p, "scuckit")):
+        sys.path.append(p)
+        break
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--backend", choices=["gpu", "cpu"], default="gpu")
+ap.add_argument("--config", default="C1")
+ap.add_argument("--time-limit", type=float, default=1500.0)
+ap.add_argument("--out", default=None)
+a = ap.parse_args()
+
+from scuckit import driver, parse_instance  # noqa: E402
+
+from paper_2510_10891_b200 import scuc  # noqa: E402
+
+doc = scuc.generate_instance(**scuc.CONFIGS[a.config])
+inst = parse_instance(doc)
+if a.backend == "gpu":
+    from paper_2510_10891_b200 import hprlp
+    hprlp.install()
+t0 = time.perf_counter()
+rep = driver.run(inst, driver.DriverConfig(time_limit=a.time_limit))
+wall = time.perf_counter() - t0
+d = rep.to_json_dict()
+out = {"backend": a.backend, "config": a.config, "time_limit_s": a.time_limit,
+       "wall_s": wall, "status": d["status"], "exit_code": d["exit_code"],
+       "objective": d["objective"], "timings": d["timings"], "nodes_total": d["nodes_total"],
+       "fixing": d["fixing"], "passes": d["passes"], "monitored_rows": len(d["monitored"]),
+       "host_cores": os.cpu_count()}
+line = json.dumps(out)
+print(line, flush=True)
+if a.out:
+    with open(a.out, "w") as fh:
+        fh.write(line + "\n")
