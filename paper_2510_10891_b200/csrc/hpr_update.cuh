@@ -41,6 +41,7 @@ struct PrimalArgs {
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
+    pdl_enter();
     const double td = halpern_t(a.ctrl, a.j_in_block);
     const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
     const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
@@ -104,6 +105,7 @@ __device__ __forceinline__ DualRow<T> dual_row(T y, T rhs, T ay, T ax, bool ineq
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
+    pdl_enter();
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i >= a.m) return;
     const double td = halpern_t(a.ctrl, a.j_in_block);
@@ -168,6 +170,7 @@ struct CheckRowsArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(TPB) k_check_rows(CheckRowsArgs<T> a) {
+    pdl_enter();
     Acc<KR> acc;
     acc.zero();
     for (int f = blockIdx.x * TPB + threadIdx.x; f < a.nf; f += gridDim.x * TPB) {
@@ -202,6 +205,7 @@ struct CheckColsArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(TPB) k_check_cols(CheckColsArgs<T> a) {
+    pdl_enter();
     Acc<KC> acc;
     acc.zero();
     for (int j = blockIdx.x * TPB + threadIdx.x; j < a.n; j += gridDim.x * TPB) {
