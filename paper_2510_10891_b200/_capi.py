@@ -112,6 +112,9 @@ def load(path: str | None = None):
     path = path or os.environ.get("HPR_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: run __graft_entry__.build() (or make) first")
+    # torch first: the library's libnccl.so.2 dependency must resolve to the NCCL
+    # torch bundles (loading the system NCCL first breaks a later `import torch`)
+    import torch  # noqa: F401
     lib = C.CDLL(path)
     lib.hpr_abi_version.restype = C.c_int32
     lib.hpr_last_error.restype = C.c_char_p

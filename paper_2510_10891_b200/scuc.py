@@ -89,8 +89,15 @@ def _dc_flows(n_b, fb, tb, react, injections, ref=0):
 
 def generate_instance(n_buses: int, n_gens: int, n_lines: int, n_periods: int,
                       seed: int = 0, n_contingencies: int = 0,
-                      name: str | None = None) -> dict:
-    """Seeded synthetic SCUC instance as a reference-schema JSON document."""
+                      name: str | None = None, shutdown_feasible: bool = False) -> dict:
+    """Seeded synthetic SCUC instance as a reference-schema JSON document.
+
+    shutdown_feasible caps every committed unit's initial output at its
+    shutdown limit, so switching it off in period 0 stays feasible (the
+    ramp-down row at t = 0, formulation.py:331-341); without it, rounding a
+    fractional u_0 to 0 can make the fixed model infeasible, which aborts the
+    reference driver (fixing.py:154-160).  The default keeps the fixtures'
+    instances unchanged."""
     if n_lines < n_buses - 1:
         raise ValueError("need at least n_buses - 1 lines for a connected network")
     rng = np.random.default_rng(seed)
@@ -143,6 +150,8 @@ def generate_instance(n_buses: int, n_gens: int, n_lines: int, n_periods: int,
         cst = [float(c0[g]) * f for f in (1.0, 1.15, 1.3)][: len(caps)]
         su = max(lo, round(0.6 * hi, 3))
         ip = round(lo + init_frac[g] * 0.5 * (hi - lo), 3) if on[g] else 0.0
+        if shutdown_feasible:
+            ip = min(ip, su)
         gens.append({
             "id": f"g{g}", "bus": f"b{int(gbus[g])}", "p_min": lo, "p_max": hi,
             "segments": [{"p_max": c, "cost": round(k, 6)} for c, k in zip(caps, cst)],

@@ -1,0 +1,49 @@
+"""Launch-shape variants of the engine must not change a single bit:
+programmatic dependent launch (HPR_PDL) and the eager block loop (HPR_EAGER)
+only change how the same kernels are scheduled, so the solve output is
+compared by digest across fresh processes (the switches are read once per
+process)."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2510_10891_b200 import hprlp, scuc
+doc, mon, lpa = scuc.build_config("C3", n_triples=60)
+eng = hprlp.Engine(lpa.to_lp())
+cfg = hprlp.SolverConfig(tolerance=1e-9, ruiz=False, max_iterations=640, log_residuals=True)
+x, y, z, st, log = eng.solve_raw(cfg)
+h = hashlib.sha256()
+for a in (x, y, z):
+    h.update(np.ascontiguousarray(a).tobytes())
+h.update(repr([(r.rel_primal, r.rel_dual, r.rel_gap, r.sigma) for r in log]).encode())
+h.update(repr((st.iterations, st.restarts, st.sigma_final)).encode())
+print("DIGEST", h.hexdigest(), st.iterations)
+""" % ROOT
+
+
+def _digest(env):
+    e = dict(os.environ)
+    e.update(env)
+    out = subprocess.run([sys.executable, "-c", SCRIPT], env=e, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("DIGEST")][-1]
+    return line.split()[1:]
+
+
+def test_launch_variants_bit_identical():
+    base = _digest({"HPR_PDL": "0"})
+    assert base[1] == "640"
+    assert _digest({"HPR_PDL": "1"}) == base
+    assert _digest({"HPR_EAGER": "1"}) == base

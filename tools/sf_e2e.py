@@ -28,13 +28,15 @@ ap.add_argument("--backend", choices=["gpu", "cpu"], default="gpu")
 ap.add_argument("--config", default="C1")
 ap.add_argument("--time-limit", type=float, default=1500.0)
 ap.add_argument("--out", default=None)
+ap.add_argument("--shutdown-feasible", action="store_true",
+                help="cap initial outputs at the shutdown limit (scuc.generate_instance)")
 a = ap.parse_args()
 
 from scuckit import driver, parse_instance  # noqa: E402
 
 from paper_2510_10891_b200 import scuc  # noqa: E402
 
-doc = scuc.generate_instance(**scuc.CONFIGS[a.config])
+doc = scuc.generate_instance(**scuc.CONFIGS[a.config], shutdown_feasible=a.shutdown_feasible)
 inst = parse_instance(doc)
 if a.backend == "gpu":
     from paper_2510_10891_b200 import hprlp
@@ -43,7 +45,8 @@ t0 = time.perf_counter()
 rep = driver.run(inst, driver.DriverConfig(time_limit=a.time_limit))
 wall = time.perf_counter() - t0
 d = rep.to_json_dict()
-out = {"backend": a.backend, "config": a.config, "time_limit_s": a.time_limit,
+out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown_feasible,
+       "time_limit_s": a.time_limit,
        "wall_s": wall, "status": d["status"], "exit_code": d["exit_code"],
        "objective": d["objective"], "timings": d["timings"], "nodes_total": d["nodes_total"],
        "fixing": d["fixing"], "passes": d["passes"], "monitored_rows": len(d["monitored"]),
