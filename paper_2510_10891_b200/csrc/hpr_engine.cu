@@ -101,6 +101,33 @@ static bool pdl_enabled() {
     return on;
 }
 
+// Small LPs run latency-bound (every kernel is a single wave whose time is one
+// CTA's dependency chain), so below FUSED_MAX_TILES tiles per product the
+// row-wise updates become SpMV epilogues: 2 kernels per iteration instead of 4
+// (C1: 22.3 -> 19.2 us per iteration; already slower at C2 + 500 triples,
+// 16.1 -> 17.0, whose 62-register epilogue kernels halve occupancy).
+// HPR_FUSED=0/1 forces the choice.
+constexpr int FUSED_MAX_TILES = 1280;
+static int fused_mode() {
+    static const int mode = [] {
+        const char* e = getenv("HPR_FUSED");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return mode;
+}
+
+// HPR_PLAIN=1: the single-GPU block body as a plain graph relaunched by the
+// host after each block (the partitioned loop), instead of the conditional
+// WHILE node — for measuring launch behaviour (e.g. with HPR_PDL) outside
+// conditional bodies.
+static bool plain_graph() {
+    static const bool on = [] {
+        const char* e = getenv("HPR_PLAIN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // cudaLaunchKernelEx wrapper (typed arguments, error check)
 template <typename... KArgs, typename... Args>
 void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
@@ -303,6 +330,7 @@ struct hpr_handle {
     int world = 1, rank = 0;
     int* d_flag = nullptr;                   // collective stop flag (time limit)
     int flags = 0;                           // hpr_options.flags
+    bool fused = false;                      // updates as SpMV epilogues (small LPs)
 };
 
 namespace {
@@ -742,6 +770,17 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
 
 template <typename T, bool CHECK>
 void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
+    if (h->fused) {
+        // small LPs: the row-wise updates ride on the products' epilogues (2 kernels)
+        PrimalArgs<T> pa{h->ctrl, j, h->n, nullptr, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo,
+                         p.up, p.BX, p.BZ, h->XM, h->ZM, h->cs};
+        launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, EpiPrimal<T, CHECK>{pa, nullptr}, s,
+                    p.f_vals);
+        DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, nullptr, p.Y, p.AY, p.rhs, p.YF,
+                       p.BY, p.BYF, h->YM, h->YMF, h->rs, h->frow};
+        launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, CHECK>{da, nullptr}, s);
+        return;
+    }
     EpiStore<T> st{p.P, nullptr};
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals);             // A^T y
     allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
@@ -776,7 +815,7 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     CK(cudaGraphCreate(&h->graph, 0));
     cudaGraph_t body = h->graph;
     cudaGraphConditionalHandle cond = 0;
-    if (!h->comm) {
+    if (!h->comm && !plain_graph()) {
         CK(cudaGraphConditionalHandleCreate(&cond, h->graph, 1, cudaGraphCondAssignDefault));
         cudaGraphNodeParams np = {};
         np.type = cudaGraphNodeTypeConditional;
@@ -853,7 +892,7 @@ double run_loop_partitioned(hpr_handle* h, double time_left) {
 }
 
 double run_loop(hpr_handle* h, double time_left = -1.0) {
-    if (h->comm) return run_loop_partitioned(h, time_left);
+    if (h->comm || plain_graph()) return run_loop_partitioned(h, time_left);
     cudaStream_t s = h->stream;
     unsigned long long cv = h->gcond;
     CK(cudaMemcpyAsync(&h->ctrl->cond, &cv, sizeof(cv), cudaMemcpyHostToDevice, s));
@@ -1485,6 +1524,11 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         plan_tiles(h, h->AT, n, m, nnz);
         plan_tiles(h, h->F, h->nf, n, f_nnz);
         plan_tiles(h, h->FT, n, h->nf, ft_nnz, h->panels ? h->pinfo : nullptr);
+        {
+            const int fm = fused_mode();
+            h->fused = !h->comm && (fm == 1 || (fm < 0 && std::max(h->F.ntiles, h->FT.ntiles) <=
+                                                              FUSED_MAX_TILES));
+        }
         phase("tiles");
         put_vec(h, h->rhs_m, p->rhs, m, true);
         put_vec(h, h->cost_m, p->cost, n, false);

@@ -67,7 +67,7 @@ __device__ __forceinline__ void block_store(Acc<K>& acc, double* part, int nslot
 }
 
 template <typename T, class Epi>
-__global__ void __launch_bounds__(TPB, 16) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
+__global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
     pdl_enter();
     __shared__ T prod[TILE_NNZ];
     __shared__ int sptr[TILE_ROWS + 1];
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(TPB, 16) k_spmv(Csr<T> A, const T* __restrict_
 template <typename T>
 struct EpiStore {
     static constexpr int K = 0;
+    static constexpr int MIN_CTAS = 16;
     T* out;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { out[r] = s; }
@@ -255,6 +256,7 @@ struct EpiStore {
 // power method step: out = A u, plus sum(out^2) for ||A A^T v|| (lp_kernel.py:157-158)
 struct EpiPower {
     static constexpr int K = 1;
+    static constexpr int MIN_CTAS = 16;
     double* out;
     double* part;
     __device__ __forceinline__ void apply(int r, double s, Acc<1>& a) {

@@ -40,32 +40,46 @@ struct PrimalArgs {
 };
 
 template <typename T, bool CHECK>
-__global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
-    pdl_enter();
+__device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
     const double td = halpern_t(a.ctrl, a.j_in_block);
     const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
-    const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
-    const int j = blockIdx.x * TPB + threadIdx.x;
-    if (j < a.n) {
-        const T x = a.X[j], z = a.Z[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
-        const T ax = a.AX[j], az = a.AZ[j], p = a.aty[j];
-        const T g = x + sig * (p - c);
-        const T bx = np_clip(g, lo, up);
-        const T bz = (bx - g) / sig;
-        const T xt = T(2) * bx - x;
-        const T zh = T(2) * bz - z;
-        a.XT[j] = xt;
-        a.X[j] = t * ax + omt * xt;
-        a.Z[j] = t * az + omt * zh;
-        if constexpr (CHECK) {
-            a.BX[j] = bx;
-            a.BZ[j] = bz;
-            const double cs = a.CS[j];
-            a.XM[j] = ((double)bx * cs) * bsc;
-            a.ZM[j] = ((double)bz * csc) / cs;
-        }
+    const T x = a.X[j], z = a.Z[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
+    const T ax = a.AX[j], az = a.AZ[j];
+    const T g = x + sig * (p - c);
+    const T bx = np_clip(g, lo, up);
+    const T bz = (bx - g) / sig;
+    const T xt = T(2) * bx - x;
+    const T zh = T(2) * bz - z;
+    a.XT[j] = xt;
+    a.X[j] = t * ax + omt * xt;
+    a.Z[j] = t * az + omt * zh;
+    if constexpr (CHECK) {
+        const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
+        a.BX[j] = bx;
+        a.BZ[j] = bz;
+        const double cs = a.CS[j];
+        a.XM[j] = ((double)bx * cs) * bsc;
+        a.ZM[j] = ((double)bz * csc) / cs;
     }
 }
+
+template <typename T, bool CHECK>
+__global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
+    pdl_enter();
+    const int j = blockIdx.x * TPB + threadIdx.x;
+    if (j < a.n) primal_col<T, CHECK>(a, j, a.aty[j]);
+}
+
+// the primal update as the epilogue of the A^T y product (small LPs, where a
+// kernel boundary costs more than the occupancy the epilogue's registers take)
+template <typename T, bool CHECK>
+struct EpiPrimal {
+    static constexpr int K = 0;
+    static constexpr int MIN_CTAS = 8;
+    PrimalArgs<T> a;
+    double* part;
+    __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { primal_col<T, CHECK>(a, r, s); }
+};
 
 // ---------------------------------------------------------------------------
 // dual half of hpr_iterate, one row i per thread (hprlp.py:193-194, 197, 202):
@@ -87,6 +101,7 @@ struct DualArgs {
     T *BY, *BYF;                // CHECK
     double *YM, *YMF;           // CHECK: master bar y and its folded form
     const double* RS;
+    const int* frow;            // nf + 1 folded-row starts (EpiDual)
 };
 
 template <typename T>
@@ -139,6 +154,46 @@ __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
         }
     }
 }
+
+// the dual update of folded row f (both rows of a twin pair) as the epilogue
+// of the A x~ product; same operations as k_update_dual
+template <typename T, bool CHECK>
+struct EpiDual {
+    static constexpr int K = 0;
+    static constexpr int MIN_CTAS = 8;
+    DualArgs<T> a;
+    double* part;
+    __device__ __forceinline__ void apply(int f, T s, Acc<0>&) {
+        const double td = halpern_t(a.ctrl, a.j_in_block);
+        const T inv = (T)(1.0 / (a.ctrl->lam * a.ctrl->sigma)), t = (T)td, omt = (T)(1.0 - td);
+        const int i = a.frow[f];
+        const bool pair = a.frow[f + 1] - i == 2;
+        const DualRow<T> r = dual_row(a.Y[i], a.RHS[i], a.AY[i], s, i >= a.n_eq, inv, t, omt);
+        DualRow<T> r2{T(0), T(0)};
+        if (pair) {
+            r2 = dual_row(a.Y[i + 1], a.RHS[i + 1], a.AY[i + 1], -s, i + 1 >= a.n_eq, inv, t, omt);
+            a.Y[i + 1] = r2.yn;
+        }
+        a.Y[i] = r.yn;
+        a.YF[f] = pair ? r.yn - r2.yn : r.yn;
+        if constexpr (CHECK) {
+            const double csc = a.ctrl->c_scale;
+            a.BY[i] = r.by;
+            const double ym = ((double)r.by * a.RS[i]) * csc;
+            a.YM[i] = ym;
+            if (pair) {
+                a.BY[i + 1] = r2.by;
+                const double ym2 = ((double)r2.by * a.RS[i + 1]) * csc;
+                a.YM[i + 1] = ym2;
+                a.BYF[f] = r.by - r2.by;
+                a.YMF[f] = ym - ym2;
+            } else {
+                a.BYF[f] = r.by;
+                a.YMF[f] = ym;
+            }
+        }
+    }
+};
 
 // y_fold / bar_y_fold / y_m_fold from unfolded vectors (any pointer may be null)
 template <typename T>
