@@ -65,29 +65,62 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled every 5 ms during
+    the timed region through NVML (the same counters nvidia-smi reports);
+    falls back to nvidia-smi polling when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.active = [], [], set()
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while True:
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+            self.mx.append(float(mx))
+            bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for name, attr in self.REASONS:
+                if bits & getattr(N, attr):
+                    self.active.add(name)
+            if self._stop.wait(0.005):
+                break
+        N.nvmlShutdown()
+
+    def _smi(self):
+        while True:
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
+                r = [v.strip() for v in out.split(",")]
+                self.sm.append(float(r[0]))
+                self.mx.append(float(r[1]))
+                for k, (name, _) in enumerate(self.REASONS):
+                    if r[2 + k].lower() == "active":
+                        self.active.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            if self._stop.wait(0.2):
+                break
+
+    def _run(self):
+        try:
+            self._nvml()
+        except Exception:
+            self._smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -99,16 +132,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.active), "samples": len(self.sm)}
 
 
 def measured_peak_hbm():

@@ -262,22 +262,35 @@ k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int 
              int mode) {
     pdl_enter();
     __shared__ double sums[KR + KC];
-    __shared__ double w[CTRL_TPB / 32];
-    for (int q = 0; q < KR + KC; ++q) {
-        const double* p = q < KR ? rowpart + (size_t)q * nr : colpart + (size_t)(q - KR) * nc;
-        const int ns = q < KR ? nr : nc;
-        double s = 0.0;
-        for (int i = threadIdx.x; i < ns; i += CTRL_TPB) s += p[i];
-        s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int k = 0; k < CTRL_TPB / 32; ++k) t += w[k];
-            sums[q] = t;
+    __shared__ double w[KR + KC][CTRL_TPB / 32];
+    // all KR + KC slot arrays in one pass (loads of every array in flight
+    // together); per array the same per-thread order and trees as one pass
+    // per array, so the sums are unchanged
+    double acc[KR + KC];
+#pragma unroll
+    for (int q = 0; q < KR + KC; ++q) acc[q] = 0.0;
+    for (int i = threadIdx.x; i < max(nr, nc); i += CTRL_TPB) {
+        if (i < nr) {
+#pragma unroll
+            for (int q = 0; q < KR; ++q) acc[q] += rowpart[(size_t)q * nr + i];
         }
-        __syncthreads();
+        if (i < nc) {
+#pragma unroll
+            for (int q = 0; q < KC; ++q) acc[KR + q] += colpart[(size_t)q * nc + i];
+        }
     }
+#pragma unroll
+    for (int q = 0; q < KR + KC; ++q) {
+        const double s = warp_sum(acc[q]);
+        if ((threadIdx.x & 31) == 0) w[q][threadIdx.x >> 5] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < KR + KC) {
+        double t = 0.0;
+        for (int k = 0; k < CTRL_TPB / 32; ++k) t += w[threadIdx.x][k];
+        sums[threadIdx.x] = t;
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
 
     const double s_p = sums[0], s_ry = sums[1], s_dy = sums[2], nf_y = sums[3];
