@@ -331,6 +331,7 @@ struct hpr_handle {
     int* d_flag = nullptr;                   // collective stop flag (time limit)
     int flags = 0;                           // hpr_options.flags
     bool fused = false;                      // updates as SpMV epilogues (small LPs)
+    bool upd_z = false;                      // Halpern z update (hpr_iterate API only)
 };
 
 namespace {
@@ -773,7 +774,7 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
     if (h->fused) {
         // small LPs: the row-wise updates ride on the products' epilogues (2 kernels)
         PrimalArgs<T> pa{h->ctrl, j, h->n, nullptr, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo,
-                         p.up, p.BX, p.BZ, h->XM, h->ZM, h->cs};
+                         p.up, p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
         launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, EpiPrimal<T, CHECK>{pa, nullptr}, s,
                     p.f_vals);
         DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, nullptr, p.Y, p.AY, p.rhs, p.YF,
@@ -785,7 +786,7 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals);             // A^T y
     allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                     p.BX, p.BZ, h->XM, h->ZM, h->cs};
+                     p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
     launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
     launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s);                         // A x~
     DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
@@ -1742,7 +1743,14 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
         k_fold_rows<T><<<nblk(h->nf), TPB, 0, s>>>(h->nf, h->frow, p.Y, p.YF, nullptr, nullptr,
                                                     nullptr, nullptr);
         CKL();
-        enqueue_iteration<T>(h, p, 0, true, s);
+        h->upd_z = true;             // the caller reads the new z
+        try {
+            enqueue_iteration<T>(h, p, 0, true, s);
+        } catch (...) {
+            h->upd_z = false;
+            throw;
+        }
+        h->upd_z = false;
     };
     if (fp32) step(float(0));
     else step(double(0));
@@ -1861,7 +1869,7 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
         Ptrs<T> p = ptrs<T>(h);
         EpiStore<T> st{p.P, nullptr};
         PrimalArgs<T> pa{h->ctrl, 0, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                         p.BX, p.BZ, h->XM, h->ZM, h->cs};
+                         p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
         DualArgs<T> da{h->ctrl, 0, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                        p.BY, p.BYF, h->YM, h->YMF, h->rs};
         switch (which) {

@@ -37,22 +37,31 @@ struct PrimalArgs {
     T *BX, *BZ;                 // CHECK: bar iterates (work dtype)
     double *XM, *ZM;            // CHECK: master-space bars (to_master, hprlp.py:272-276)
     const double* CS;
+    // Halpern update of the current z (hprlp.py:198, 203).  Nothing in a solve
+    // reads it: bar_z depends on x and y only, the KKT check, the sigma update
+    // and the restart test use the bars, and a restart overwrites z with
+    // bar_z (:168-174).  The solve loop therefore skips it (3 of the 11 vectors
+    // of this pass); hpr_iterate (the single-step API, whose caller sees z)
+    // keeps it.
+    bool upd_z;
 };
 
 template <typename T, bool CHECK>
 __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
     const double td = halpern_t(a.ctrl, a.j_in_block);
     const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
-    const T x = a.X[j], z = a.Z[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
-    const T ax = a.AX[j], az = a.AZ[j];
+    const T x = a.X[j], c = a.C[j], lo = a.LO[j], up = a.UP[j];
+    const T ax = a.AX[j];
     const T g = x + sig * (p - c);
     const T bx = np_clip(g, lo, up);
     const T bz = (bx - g) / sig;
     const T xt = T(2) * bx - x;
-    const T zh = T(2) * bz - z;
     a.XT[j] = xt;
     a.X[j] = t * ax + omt * xt;
-    a.Z[j] = t * az + omt * zh;
+    if (a.upd_z) {
+        const T zh = T(2) * bz - a.Z[j];
+        a.Z[j] = t * a.AZ[j] + omt * zh;
+    }
     if constexpr (CHECK) {
         const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
         a.BX[j] = bx;
