@@ -36,15 +36,6 @@ __device__ __forceinline__ bool finite(float v) { return isfinite(v); }
 template <typename T> __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
 template <typename T> __device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }
 
-// Programmatic dependent launch (HPR_PDL=1, hpr_engine.cu): every kernel of
-// the loop body waits for its predecessor grid before touching memory, then
-// lets its own dependents launch, so the next grid is resident when this one
-// drains.  Both instructions are no-ops for launches without the attribute.
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
 // Solver control block, resident in device memory for the whole solve.  The
 // iteration kernels read sigma/lam/k0 from it; the controller kernel owns it.
 struct Ctrl {

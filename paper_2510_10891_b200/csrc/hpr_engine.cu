@@ -90,17 +90,6 @@ inline int nblk(long long n, int tpb = TPB) {
     return (int)std::max<long long>(1, (n + tpb - 1) / tpb);
 }
 
-// Programmatic dependent launch of the loop-body kernels (set while the block
-// graph is captured; HPR_PDL=1 enables it).
-static thread_local bool g_pdl = false;
-static bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("HPR_PDL");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 // Small LPs run latency-bound (every kernel is a single wave whose time is one
 // CTA's dependency chain), so below FUSED_MAX_TILES tiles per product the
 // row-wise updates become SpMV epilogues: 2 kernels per iteration instead of 4
@@ -118,8 +107,7 @@ static int fused_mode() {
 
 // HPR_PLAIN=1: the single-GPU block body as a plain graph relaunched by the
 // host after each block (the partitioned loop), instead of the conditional
-// WHILE node — for measuring launch behaviour (e.g. with HPR_PDL) outside
-// conditional bodies.
+// WHILE node (measurement aid).
 static bool plain_graph() {
     static const bool on = [] {
         const char* e = getenv("HPR_PLAIN");
@@ -135,13 +123,6 @@ void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&.
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    if (g_pdl) {
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-    }
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
     if (e == cudaSuccess && sync_debug() && !g_capturing) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -831,18 +812,15 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
     CK(cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
     g_capturing = true;
-    g_pdl = pdl_enabled() && !h->comm;
     try {
         for (int j = 0; j < B; ++j) enqueue_iteration<T>(h, p, j, j == B - 1, h->cap);
         enqueue_check<T>(h, p, 1, h->cap);
     } catch (...) {
-        g_pdl = false;
         g_capturing = false;
         cudaGraph_t dummy;
         cudaStreamEndCapture(h->cap, &dummy);
         throw;
     }
-    g_pdl = false;
     g_capturing = false;
     cudaGraph_t captured;
     CK(cudaStreamEndCapture(h->cap, &captured));

@@ -260,7 +260,6 @@ constexpr int CTRL_TPB = 512;
 __global__ void __launch_bounds__(CTRL_TPB)
 k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int nc, LogRec* log,
              int mode) {
-    pdl_enter();
     __shared__ double sums[KR + KC];
     __shared__ double w[KR + KC][CTRL_TPB / 32];
     // all KR + KC slot arrays in one pass (loads of every array in flight
@@ -411,7 +410,6 @@ __global__ void k_restart_copy(const Ctrl* c, int n, int m, int nf, const double
                                const double* YM, const double* ZM, double* BXm, double* BYm,
                                double* BZm, T* X, T* Y, T* Z, T* AX, T* AY, T* AZ, const T* BX,
                                const T* BY, const T* BZ, T* YF, const T* BYF) {
-    pdl_enter();
     const int imp = c->flag_improved, rst = c->flag_restart;
     if (!imp && !rst) return;
     const int len = n > m ? n : m;

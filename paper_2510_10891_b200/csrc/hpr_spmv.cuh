@@ -68,7 +68,6 @@ __device__ __forceinline__ void block_store(Acc<K>& acc, double* part, int nslot
 
 template <typename T, class Epi>
 __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
-    pdl_enter();
     __shared__ T prod[TILE_NNZ];
     __shared__ int sptr[TILE_ROWS + 1];
     __shared__ T wpart[TPB / 32];

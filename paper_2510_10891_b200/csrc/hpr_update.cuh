@@ -74,7 +74,6 @@ __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
-    pdl_enter();
     const int j = blockIdx.x * TPB + threadIdx.x;
     if (j < a.n) primal_col<T, CHECK>(a, j, a.aty[j]);
 }
@@ -129,7 +128,6 @@ __device__ __forceinline__ DualRow<T> dual_row(T y, T rhs, T ay, T ax, bool ineq
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
-    pdl_enter();
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i >= a.m) return;
     const double td = halpern_t(a.ctrl, a.j_in_block);
@@ -234,7 +232,6 @@ struct CheckRowsArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(TPB) k_check_rows(CheckRowsArgs<T> a) {
-    pdl_enter();
     Acc<KR> acc;
     acc.zero();
     for (int f = blockIdx.x * TPB + threadIdx.x; f < a.nf; f += gridDim.x * TPB) {
@@ -269,7 +266,6 @@ struct CheckColsArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(TPB) k_check_cols(CheckColsArgs<T> a) {
-    pdl_enter();
     Acc<KC> acc;
     acc.zero();
     for (int j = blockIdx.x * TPB + threadIdx.x; j < a.n; j += gridDim.x * TPB) {

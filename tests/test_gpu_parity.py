@@ -306,6 +306,23 @@ def test_index_free_flow_rows(H):
         np.testing.assert_allclose(a[k], b[k], rtol=1e-7, atol=1e-9)
 
 
+def test_c1_tol_1e6_numerical_failure_matches_reference(H):
+    """C1 at tolerance 1e-6: the reference's own solve ends in
+    numerical-failure at iteration 187,408 after 548 restarts (its dual iterate
+    overflows; tests/golden/c1_1e6.json, ~17 min on the CPU).  The engine must
+    fail at the same iteration, with the same best objective."""
+    import json
+    import os
+    from paper_2510_10891_b200 import scuc
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_1e6.json")))
+    doc = scuc.generate_instance(**scuc.CONFIGS["C1"])
+    lpa = scuc.build_relaxation(doc, scuc.all_base_triples(doc))
+    r = H.solve(lpa.to_lp(), H.SolverConfig(tolerance=1e-6, ruiz=False, max_iterations=400000))
+    assert r.status.value == g["status"]
+    assert r.iterations == g["iterations"] and r.restarts == g["restarts"]
+    assert abs(r.objective - g["objective"]) <= 1e-9 * abs(g["objective"])
+
+
 def test_c1_against_reference_trajectory(H):
     """C1 (118-bus, all base flow rows; 24,504 x 13,200, 1.87M nnz) to 1e-4,
     against the reference's own FP64/FP32 runs (tests/golden/c1_trajectory.json,

@@ -1,6 +1,6 @@
 """Launch-shape variants of the engine must not change a single bit:
-programmatic dependent launch (HPR_PDL), the eager block loop (HPR_EAGER) and
-the small-LP fused iteration (HPR_FUSED: the row-wise updates as SpMV
+the eager block loop (HPR_EAGER), the plain host-relaunched graph (HPR_PLAIN)
+and the small-LP fused iteration (HPR_FUSED: the row-wise updates as SpMV
 epilogues) only change how the same operations are scheduled, so the solve output is
 compared by digest across fresh processes (the switches are read once per
 process)."""
@@ -44,9 +44,9 @@ def _digest(env):
 
 
 def test_launch_variants_bit_identical():
-    base = _digest({"HPR_PDL": "0", "HPR_FUSED": "0"})
+    base = _digest({"HPR_FUSED": "0"})
     assert base[1] == "640"
-    assert _digest({"HPR_PDL": "1", "HPR_FUSED": "0"}) == base
+    assert _digest({"HPR_PLAIN": "1", "HPR_FUSED": "0"}) == base
     assert _digest({"HPR_EAGER": "1", "HPR_FUSED": "0"}) == base
     assert _digest({"HPR_FUSED": "1"}) == base
     assert _digest({"HPR_FUSED": "1", "HPR_EAGER": "1"}) == base
