@@ -32,7 +32,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -410,6 +412,10 @@ struct Scratch {
 // Host -> device upload of a pageable array through two pinned bounce
 // buffers (host memcpy of chunk k+1 overlaps the DMA of chunk k); several
 // times faster than a pageable cudaMemcpy for the 0.5 GB CSR of C4.
+// Pageable host -> device through a pinned double buffer: host threads stage
+// chunk k+1 while the DMA engine moves chunk k.  The pinned buffer is kept for
+// the process (pinning 64 MB costs 30-100 ms, and releasing it sometimes
+// blocks for ~0.5 s), shared by all handles under a mutex.
 void upload_pageable(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     constexpr size_t CH = 32u << 20;
     if (bytes < 2 * CH) {
@@ -417,16 +423,34 @@ void upload_pageable(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         CK(cudaStreamSynchronize(s));
         return;
     }
-    char* buf = nullptr;
-    CK(cudaMallocHost(&buf, 2 * CH));
+    static std::mutex mu;
+    static char* buf = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!buf) CK(cudaMallocHost(&buf, 2 * CH));
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     bool used[2] = {false, false};
+    // the staging memcpy is split over host threads (one core moves ~2 GB/s here)
+    const unsigned nth = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    auto stage = [&](char* to, const char* from, size_t len) {
+        if (nth == 1 || len < (4u << 20)) {
+            std::memcpy(to, from, len);
+            return;
+        }
+        std::vector<std::thread> th;
+        const size_t part = (len + nth - 1) / nth;
+        for (unsigned t = 0; t < nth; ++t) {
+            const size_t o = t * part;
+            if (o >= len) break;
+            th.emplace_back([=] { std::memcpy(to + o, from + o, std::min(part, len - o)); });
+        }
+        for (auto& x : th) x.join();
+    };
     for (size_t off = 0, k = 0; off < bytes; off += CH, k ^= 1) {
         const size_t len = std::min(CH, bytes - off);
         if (used[k]) CK(cudaEventSynchronize(ev[k]));
-        std::memcpy(buf + k * CH, (const char*)src + off, len);
+        stage(buf + k * CH, (const char*)src + off, len);
         CK(cudaMemcpyAsync((char*)dst + off, buf + k * CH, len, cudaMemcpyHostToDevice, s));
         CK(cudaEventRecord(ev[k], s));
         used[k] = true;
@@ -434,7 +458,6 @@ void upload_pageable(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
-    cudaFreeHost(buf);
 }
 
 // exclusive scan of len[0..rows) into out[0..rows] (len[rows] must be 0)
@@ -1253,6 +1276,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             cudaGetLastError();
             return d;
         };
+        phase("init");
         const int* rptr = p->indptr;
         const int* ridx = p->indices;
         const double* rval = p->data;
@@ -1271,6 +1295,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             upload_pageable(q, p->data, sizeof(double) * nnz, s);
             rval = q;
         }
+        phase("upload A");
         {
             int* bad = sc.alloc<int>(4);
             CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
@@ -1286,7 +1311,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             if (hv[0] & 1) fail(HPR_ERR_INVALID, "column index out of range");
             if (hv[0] & 2) fail(HPR_ERR_INVALID, "indptr not monotone");
         }
-        phase("stage+check");
+        phase("check");
 
         // ---- A^T: stable sort of the entries by column (rows stay ordered)
         int* iota_e = sc.alloc<int>(nnz);
