@@ -334,13 +334,26 @@ def run_b200(args):
             max_iterations=args.e2e_max_iter))
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        h2d = 2 * (4 * (max(m, n) + 1)) + 2 * nnz * 12 + 8 * (m + 3 * n)
+        h2d = 4 * (m + 1) + 12 * nnz + 8 * (m + 3 * n)     # CSR + rhs/cost/lower/upper
         out["e2e"] = {"value": res.iterations / wall, "unit": "iterations/s",
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * (2 * n + m),
                       "time_to_tol_s": wall, "status": res.status.value,
                       "iterations": res.iterations, "restarts": res.restarts,
                       "objective": res.objective, "rel_kkt": res.kkt.max_rel,
                       "loop_seconds": res.device_stats.get("loop_seconds")}
+        if args.precision == "fp64":
+            # the paper's setting (FP32 work precision, FP64 master check), same API
+            t0 = time.perf_counter()
+            r32 = hprlp.solve(lpa.to_lp(), hprlp.SolverConfig(
+                tolerance=1e-4, ruiz=False, precision=Precision("fp32"),
+                max_iterations=args.e2e_max_iter))
+            torch.cuda.synchronize()
+            w32 = time.perf_counter() - t0
+            out["e2e_fp32"] = {"time_to_tol_s": w32, "iterations": r32.iterations,
+                               "iterations_per_s": r32.iterations / w32,
+                               "status": r32.status.value, "objective": r32.objective,
+                               "rel_kkt": r32.kkt.max_rel,
+                               "fp64_fallback": bool(getattr(r32, "fp64_fallback", False))}
     if rank == 0 and not args.no_cpu_baseline:
         v, el = cpu_baseline_sample(lpa, st0.lam, st.sigma_final, args.precision)
         out["cpu_baseline"] = {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
