@@ -1,5 +1,5 @@
 import time, json, numpy as np, sys
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from paper_2510_10891_b200 import scuc, hprlp
 from paper_2510_10891_b200.lp import Precision
 t=time.time(); doc, mon, lpa = scuc.build_config("C1"); print("build", time.time()-t, lpa.shape, lpa.nnz, lpa.digest())
