@@ -66,3 +66,23 @@ def test_product_path_does_not_import_oracle():
         if fn.endswith(".py"):
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace(
                 "no CPU fallback", ""), fn
+
+
+def test_c_caller_links_and_presolves(tmp_path):
+    """tests/c/abi_smoke.c: a plain-C caller of include/*.h linked against the
+    library (the binding any host language would make); runs the host-only
+    presolve core through the C-ABI and the solver ABI's no-GPU paths."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        import pytest
+        pytest.skip("gcc not available")
+    libdir = os.path.join(ROOT, "paper_2510_10891_b200")
+    exe = str(tmp_path / "abi_smoke")
+    subprocess.run([gcc, "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "abi_smoke.c"), "-L", libdir,
+                    "-lhprlp_b200", f"-Wl,-rpath,{libdir}", "-lm", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().endswith("ok")
