@@ -219,6 +219,8 @@ typedef struct hpr_layout {
     int64_t f_nnz;             /* entries of F incl. explicit zeros padding flow rows */
     int64_t ft_nnz;            /* entries left in F^T */
     int64_t index_free_nnz_f;  /* entries of F streamed without their column index */
+    int32_t fused;             /* 1: the row-wise updates run as the products' epilogues */
+    int32_t reserved;
 } hpr_layout;
 int hpr_get_layout(hpr_handle* h, hpr_layout* out);
 
@@ -229,7 +231,9 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out);
  * launched reps times outside the graph on the handle's stream:
  * which = 0: A x~ product; 1: A^T y product; 2: primal row-wise update
  * (projection + reflection + Halpern); 3: dual row-wise update; 4: one KKT
- * check block (mutates the solver state: call after the measurements). */
+ * check block (mutates the solver state: call after the measurements);
+ * 5: A^T y product with the primal update as epilogue; 6: A x~ product with the
+ * dual update as epilogue (the fused iteration's two kernels). */
 int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* stats);
 int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds_per_launch);
 

@@ -92,13 +92,16 @@ inline int nblk(long long n, int tpb = TPB) {
     return (int)std::max<long long>(1, (n + tpb - 1) / tpb);
 }
 
-// Small LPs run latency-bound (every kernel is a single wave whose time is one
-// CTA's dependency chain), so below FUSED_MAX_TILES tiles per product the
-// row-wise updates become SpMV epilogues: 2 kernels per iteration instead of 4
-// (C1: 22.3 -> 19.2 us per iteration; already slower at C2 + 500 triples,
-// 16.1 -> 17.0, whose 62-register epilogue kernels halve occupancy).
-// HPR_FUSED=0/1 forces the choice.
-constexpr int FUSED_MAX_TILES = 1280;
+// Fused iteration: the row-wise updates run as the epilogues of the two
+// products (2 kernels per iteration instead of 4; EpiPrimal / EpiDual, held to
+// 32 registers so the products keep 16 CTAs/SM).  Same operations, same bits.
+// Measured per iteration: C1 21.9 -> 19.3 us, C2 + 500 triples 15.7 -> 13.5,
+// C3 + 2000 triples 62.7 -> 60.4, C4 174.2 -> 174.1.  The fused kernels are
+// slower than the split pair (C4: 83.6 vs 61.4 + 14.6 us), so the win is the
+// two saved kernel boundaries, which stops paying at C4 size: fused is chosen
+// below FUSED_MAX_TILES tiles per product.  HPR_FUSED=0/1 forces the choice
+// (the partitioned mode is always split: A^T y is all-reduced first).
+constexpr int FUSED_MAX_TILES = 20000;
 static int fused_mode() {
     static const int mode = [] {
         const char* e = getenv("HPR_FUSED");
@@ -1815,6 +1818,7 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
     out->workspace_bytes = h->ws_bytes;
     out->panel_cols = h->panel_cols;
     out->panel_nnz = h->panel_nnz;
+    out->fused = h->fused ? 1 : 0;
     out->f_nnz = h->F.nnz;
     out->ft_nnz = h->FT.nnz;
     out->index_free_nnz_f = h->F.free_nnz;
@@ -1861,7 +1865,7 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     API_BEGIN
     if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
-    if (which < 0 || which > 4) fail(HPR_ERR_INVALID, "unknown kernel");
+    if (which < 0 || which > 6) fail(HPR_ERR_INVALID, "unknown kernel");
     CK(cudaSetDevice(h->dev));
     cudaStream_t s = h->stream;
     // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update,
@@ -1880,6 +1884,17 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
             case 1: launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals); break;
             case 2: k_update_primal<T, false><<<nblk(h->n), TPB, 0, s>>>(pa); break;
             case 3: k_update_dual<T, false><<<nblk(h->m), TPB, 0, s>>>(da); break;
+            case 5: {   // fused: A^T y product + primal update (epilogue)
+                launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, EpiPrimal<T, false>{pa, nullptr},
+                            s, p.f_vals);
+                break;
+            }
+            case 6: {   // fused: A x~ product + dual update (epilogue)
+                DualArgs<T> df = da;
+                df.frow = h->frow;
+                launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, false>{df, nullptr}, s);
+                break;
+            }
             default: enqueue_check<T>(h, p, 1, s); break;
         }
         CKL();

@@ -78,12 +78,13 @@ __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
     if (j < a.n) primal_col<T, CHECK>(a, j, a.aty[j]);
 }
 
-// the primal update as the epilogue of the A^T y product (small LPs, where a
-// kernel boundary costs more than the occupancy the epilogue's registers take)
+// the primal update as the epilogue of the A^T y product (fused iteration;
+// MIN_CTAS 16 keeps the product at 32 registers — the epilogue spills a few
+// values, which costs less than the halved occupancy of 62 registers)
 template <typename T, bool CHECK>
 struct EpiPrimal {
     static constexpr int K = 0;
-    static constexpr int MIN_CTAS = 8;
+    static constexpr int MIN_CTAS = 16;
     PrimalArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { primal_col<T, CHECK>(a, r, s); }
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
 template <typename T, bool CHECK>
 struct EpiDual {
     static constexpr int K = 0;
-    static constexpr int MIN_CTAS = 8;
+    static constexpr int MIN_CTAS = 16;
     DualArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int f, T s, Acc<0>&) {
