@@ -338,7 +338,14 @@ def run_b200(args):
     if partitioned:
         out["config"]["block"] = {"rows": int(blk.rows.size), "nnz": int(blk.nnz)}
     if not args.no_e2e and not partitioned:
-        # public API from host buffers: upload + setup + solve to 1e-4 + copy back
+        # public API from host buffers: upload + setup + solve to 1e-4 + copy back.
+        # The benchmark engine is released first, so its 5.6 GB workspace returns
+        # to torch's caching allocator and the e2e engine is not charged for a
+        # second cudaMalloc the benchmark alone made necessary.
+        eng.close()
+        del eng
+        import gc
+        gc.collect()
         lp_host = lpa.to_lp()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -353,9 +360,12 @@ def run_b200(args):
                       "time_to_tol_s": wall, "status": res.status.value,
                       "iterations": res.iterations, "restarts": res.restarts,
                       "objective": res.objective, "rel_kkt": res.kkt.max_rel,
-                      "loop_seconds": res.device_stats.get("loop_seconds")}
+                      "loop_seconds": res.device_stats.get("loop_seconds"),
+                      "device_setup_seconds": res.device_stats.get("setup_seconds")}
         if args.precision == "fp64":
             # the paper's setting (FP32 work precision, FP64 master check), same API
+            del res, lp_host
+            gc.collect()
             t0 = time.perf_counter()
             r32 = hprlp.solve(lpa.to_lp(), hprlp.SolverConfig(
                 tolerance=1e-4, ruiz=False, precision=Precision("fp32"),
