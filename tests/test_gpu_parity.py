@@ -447,3 +447,26 @@ def test_two_engines_concurrently(H):
         assert abs(float(np.dot(lp.cost, o[0])) - ref.objective) <= 1e-6 * max(1, abs(ref.objective))
     for e in engs:
         e.close()
+
+
+def test_config_variants_vs_reference(H):
+    """Non-default SolverConfig fields (check cadence, restart thresholds,
+    sigma0 / damping, Ruiz passes, no Pock-Chambolle, no normalisation, power
+    settings incl. a non-converging power method, seed, iteration limits) on 8
+    random LPs against the unmodified reference's records
+    (tests/golden/config_variants.json)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config_variants.json")))
+    lps = golden_io.random_lps()[:8]
+    same = 0
+    for key, rec in g["results"].items():
+        i, name = key.split("/")
+        r = H.solve(lps[int(i)][0], H.SolverConfig(**g["variants"][name]))
+        assert r.status.value == rec["status"], key
+        assert r.lam == pytest.approx(rec["lam"], rel=1e-12), key
+        assert abs(r.objective - rec["objective"]) <= 1e-6 * max(1.0, abs(rec["objective"])), key
+        if rec["status"] == "iteration-limit":
+            assert r.iterations == rec["iterations"], key
+        same += (r.iterations, r.restarts) == (rec["iterations"], rec["restarts"])
+    assert same >= 0.9 * len(g["results"]), same

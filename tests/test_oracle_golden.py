@@ -104,3 +104,21 @@ def test_oracle_equals_reference_directly():
         b = O.solve(lp, O.OracleConfig(tolerance=1e-7, log_residuals=True))
         assert a.iterations == b.iterations and a.objective == b.objective
         assert np.array_equal(a.x, b.x) and a.residual_log == b.residual_log
+
+
+def test_oracle_config_variants_match_reference():
+    """Every SolverConfig field the driver leaves at its default, moved
+    (tests/golden/config_variants.json, unmodified reference): the oracle
+    reproduces status, iterations, restarts, lambda, sigma and the objective."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config_variants.json")))
+    lps = golden_io.random_lps()[:8]
+    for key, rec in g["results"].items():
+        i, name = key.split("/")
+        r = O.solve(lps[int(i)][0], O.OracleConfig(**g["variants"][name]))
+        assert r.status == rec["status"], key
+        assert r.iterations == rec["iterations"] and r.restarts == rec["restarts"], key
+        assert r.lam == rec["lam"], key
+        assert r.sigma_final == rec["sigma_final"], key
+        assert r.objective == rec["objective"], key
