@@ -78,3 +78,11 @@ def c1():
         return None
     with open(p) as fh:
         return json.load(fh)
+
+
+def warm_starts():
+    """[(start (x, y, z), {"fp64": rec, "fp32": rec})] for random_lps()[:6]
+    (tests/golden/make_warm_golden.py)."""
+    z = np.load(os.path.join(GOLDEN, "warm_starts.npz"))
+    meta = json.loads(bytes(z["meta"]).decode())
+    return [(tuple(z[f"lp{i}_{c}0"] for c in "xyz"), rec) for i, rec in enumerate(meta)]

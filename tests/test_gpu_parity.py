@@ -470,3 +470,21 @@ def test_config_variants_vs_reference(H):
             assert r.iterations == rec["iterations"], key
         same += (r.iterations, r.restarts) == (rec["iterations"], rec["restarts"])
     assert same >= 0.9 * len(g["results"]), same
+
+
+def test_warm_starts_vs_reference(H):
+    """Warm starts from a perturbed optimum (the B&B node pattern), FP64 and
+    FP32, against the reference's records (tests/golden/warm_starts.npz)."""
+    from paper_2510_10891_b200.lp import Precision
+    lps = golden_io.random_lps()[:6]
+    same = 0
+    for (lp, _, _), (start, rec) in zip(lps, golden_io.warm_starts()):
+        for prec, tol in (("fp64", 1e-7), ("fp32", 1e-5)):
+            r = H.solve(lp, H.SolverConfig(tolerance=tol, precision=Precision(prec)), start=start)
+            g = rec[prec]
+            assert r.status.value == g["status"]
+            assert r.lam == pytest.approx(g["lam"], rel=1e-12)
+            band = 1e-6 if prec == "fp64" else 1e-4
+            assert abs(r.objective - g["objective"]) <= band * max(1.0, abs(g["objective"]))
+            same += (r.iterations, r.restarts) == (g["iterations"], g["restarts"])
+    assert same >= 9, same

@@ -122,3 +122,17 @@ def test_oracle_config_variants_match_reference():
         assert r.lam == rec["lam"], key
         assert r.sigma_final == rec["sigma_final"], key
         assert r.objective == rec["objective"], key
+
+
+def test_oracle_warm_starts_match_reference():
+    """Solves started from a perturbed optimum (B&B's start=), FP64 and FP32,
+    against the reference's records (tests/golden/warm_starts.npz)."""
+    from paper_2510_10891_b200.lp import Precision  # noqa: F401
+    lps = golden_io.random_lps()[:6]
+    for (lp, _, _), (start, rec) in zip(lps, golden_io.warm_starts()):
+        for prec, tol in (("fp64", 1e-7), ("fp32", 1e-5)):
+            r = O.solve(lp, O.OracleConfig(tolerance=tol, precision=prec), start=start)
+            g = rec[prec]
+            assert r.status == g["status"]
+            assert (r.iterations, r.restarts) == (g["iterations"], g["restarts"])
+            assert r.objective == g["objective"] and r.lam == g["lam"]
