@@ -205,6 +205,27 @@ def make_c1():
         json.dump(out, fh)
 
 
+def make_c2():
+    """C2 + 500 triples: PTDF flow rows of up to ~1,900 entries, so the
+    engine's padded index-free rows and A^T y flow panels are on the path
+    (C1's ~225-entry flow rows are below both thresholds)."""
+    doc, mon, lpa = scuc.build_config("C2", n_triples=500)
+    lp = ref_lp(lpa.indptr, lpa.indices, lpa.data, lpa.shape, lpa.rhs, lpa.cost,
+                lpa.lower, lpa.upper, lpa.n_eq)
+    out = {"digest": lpa.digest(), "shape": list(lpa.shape), "nnz": lpa.nnz}
+    r = solve_record(lp, tolerance=1e-4, ruiz=False, precision=lp_kernel.Precision.FP64,
+                     log_residuals=True)
+    log = r.residual_log
+    out["fp64"] = res_dict(r) | {
+        "log": [[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"], e["rel_box"],
+                 e["rel_gap"], e["sigma"]] for e in log],
+        "solve_time_s": r.solve_time,
+    }
+    print("C2", r.status.value, r.iterations, r.restarts, r.objective, r.solve_time)
+    with open(os.path.join(HERE, "c2_trajectory.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
@@ -218,3 +239,5 @@ if __name__ == "__main__":
         make_scuc_small()
     if a.c1 or a.only == "c1":
         make_c1()
+    if a.only == "c2":
+        make_c2()

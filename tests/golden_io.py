@@ -80,6 +80,14 @@ def c1():
         return json.load(fh)
 
 
+def c2():
+    p = os.path.join(GOLDEN, "c2_trajectory.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh)
+
+
 def warm_starts():
     """[(start (x, y, z), {"fp64": rec, "fp32": rec})] for random_lps()[:6]
     (tests/golden/make_warm_golden.py)."""

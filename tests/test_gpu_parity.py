@@ -360,6 +360,42 @@ def test_c1_against_reference_trajectory(H):
             assert abs(r.objective - gg["objective"]) <= 1e-4 * abs(gg["objective"])
 
 
+def test_c2_against_reference_trajectory(H):
+    """C2 + 500 triples (75,904 x 82,416, 1.85M nnz) to 1e-4 against the
+    reference's FP64 run (tests/golden/c2_trajectory.json).  Its PTDF flow rows
+    (up to ~1,900 entries) are long enough for the padded index-free rows and
+    the A^T y flow panels, so this pins those layout paths to the reference
+    (C1's flow rows are below both thresholds)."""
+    from paper_2510_10891_b200 import scuc
+    g = golden_io.c2()
+    if g is None:
+        pytest.skip("c2_trajectory.json not generated")
+    doc, mon, lpa = scuc.build_config("C2", n_triples=500)
+    lp = lpa.to_lp()
+    eng = H.Engine(lp)
+    lay = eng.layout()
+    eng.close()
+    assert lay["panel_nnz"] > 0 and lay["f_nnz"] > lay["folded_nnz"]     # the paths are live
+    if lpa.digest() != g["digest"]:
+        cfg = dict(tolerance=1e-4, ruiz=False, max_iterations=2000, log_residuals=True)
+        ref = O.solve(lpa, O.OracleConfig(**cfg))
+        r = H.solve(lp, H.SolverConfig(**cfg))
+        assert r.lam == pytest.approx(ref.lam, rel=1e-12)
+        assert abs(r.objective - ref.objective) <= 1e-6 * abs(ref.objective)
+        return
+    gg = g["fp64"]
+    r = H.solve(lp, H.SolverConfig(tolerance=1e-4, ruiz=False, log_residuals=True))
+    assert r.status.value == gg["status"]
+    assert r.lam == pytest.approx(gg["lam"], rel=1e-12)
+    assert abs(r.iterations - gg["iterations"]) <= 0.01 * gg["iterations"]
+    assert abs(r.restarts - gg["restarts"]) <= 1
+    assert abs(r.objective - gg["objective"]) <= 1e-6 * abs(gg["objective"])
+    mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"],
+                      e["rel_box"], e["rel_gap"], e["sigma"]] for e in r.residual_log])
+    ref = np.array(gg["log"])
+    np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
+
+
 def test_partitioned_engine_single_rank(H):
     """The row-partitioned engine mode (NCCL all-reduces captured in the block
     graph, host-driven block loop, collective stop test) run with one rank
