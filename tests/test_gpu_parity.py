@@ -376,24 +376,26 @@ def test_c2_against_reference_trajectory(H):
     lay = eng.layout()
     eng.close()
     assert lay["panel_nnz"] > 0 and lay["f_nnz"] > lay["folded_nnz"]     # the paths are live
-    if lpa.digest() != g["digest"]:
+    same_lp = lpa.digest() == g["digest"]
+    if not same_lp:
+        # the box's BLAS can move the PTDF's last bits: check the on-box oracle too
         cfg = dict(tolerance=1e-4, ruiz=False, max_iterations=2000, log_residuals=True)
         ref = O.solve(lpa, O.OracleConfig(**cfg))
         r = H.solve(lp, H.SolverConfig(**cfg))
         assert r.lam == pytest.approx(ref.lam, rel=1e-12)
         assert abs(r.objective - ref.objective) <= 1e-6 * abs(ref.objective)
-        return
     gg = g["fp64"]
     r = H.solve(lp, H.SolverConfig(tolerance=1e-4, ruiz=False, log_residuals=True))
     assert r.status.value == gg["status"]
-    assert r.lam == pytest.approx(gg["lam"], rel=1e-12)
+    assert r.lam == pytest.approx(gg["lam"], rel=1e-12 if same_lp else 1e-9)
     assert abs(r.iterations - gg["iterations"]) <= 0.01 * gg["iterations"]
     assert abs(r.restarts - gg["restarts"]) <= 1
     assert abs(r.objective - gg["objective"]) <= 1e-6 * abs(gg["objective"])
-    mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"],
-                      e["rel_box"], e["rel_gap"], e["sigma"]] for e in r.residual_log])
-    ref = np.array(gg["log"])
-    np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
+    if same_lp:
+        mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"],
+                          e["rel_box"], e["rel_gap"], e["sigma"]] for e in r.residual_log])
+        ref = np.array(gg["log"])
+        np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
 
 
 def test_partitioned_engine_single_rank(H):
