@@ -90,7 +90,9 @@ typedef struct hpr_options {
      * hpr_create is this rank's row block (all n columns); the ranks of
      * nccl_comm (an ncclComm_t from hpr_nccl_comm_init) exchange the A^T y
      * partials, the column norms and the row-side check sums.  world_size
-     * <= 1 or nccl_comm == NULL is the single-GPU engine. */
+     * <= 1 or nccl_comm == NULL is the single-GPU engine.  This is the
+     * one-process-per-GPU form of SURVEY §8(b)'s hpr_create_multi(devices,
+     * ndev, comm): each rank calls hpr_create for its own device and block. */
     void* nccl_comm;
     int32_t world_size;
     int32_t rank;
