@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
                 // one row-major block: no per-row lookups between the tile and the loads
                 const T* __restrict__ pv = A.pvals + ((long long)pd.z + r);
                 const T* __restrict__ yv = xg + pd.x;
-                constexpr int U = 4;
+                // 6 rows per thread per batch (A/B: 4 -> 6 took F^T 59.5 -> 57.5 us at C4;
+                // 7 is no better, and predicated full batches spill)
+                constexpr int U = 6;
                 int q = warp;
                 for (; q + (U - 1) * (TPB / 32) < pd.y; q += U * (TPB / 32)) {
                     T v[U], g[U];
