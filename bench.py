@@ -159,6 +159,17 @@ def ncu_traffic(kernel_key):
         return None
 
 
+def workload(args):
+    """The config's description (scuc.CONFIGS; C4 + 1000 base triples is the
+    BASELINE.json headline)."""
+    from paper_2510_10891_b200 import scuc
+    c = scuc.CONFIGS[args.config]
+    n = args.triples or {"C1": -1, "C2": 500, "C3": 2000, "C4": 1000}[args.config]
+    tri = "all base flow triples" if n < 0 else f"{n} sampled base flow triples"
+    return (f"{args.config}: synthetic {c['n_buses']}-bus/{c['n_gens']}-unit/{c['n_periods']}-period "
+            f"SCUC LP relaxation + {tri}")
+
+
 def build_lp(args, device):
     from paper_2510_10891_b200 import scuc
     t = time.perf_counter()
@@ -293,8 +304,7 @@ def run_b200(args):
         "higher_is_better": True, "scaling": "strong" if partitioned else "weak",
         "vs_baseline": None,
         "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: synthetic 13659-bus/4092-unit/36-period SCUC "
-                               f"LP relaxation + {args.triples or 1000} base flow triples",
+        "config": {"workload": workload(args),
                    "rows": m, "cols": n, "nnz": nnz, "step": "16 HPR iterations + KKT check",
                    "device_layout": {"folded_rows": lay["folded_rows"],
                                      "folded_nnz": lay["folded_nnz"],
@@ -437,8 +447,7 @@ def run_reference(args):
            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
            "data": "synthetic",
-           "config": {"workload": f"{args.config}: synthetic 13659-bus SCUC LP relaxation + "
-                                  f"{args.triples or 1000} base flow triples",
+           "config": {"workload": workload(args),
                       "rows": m, "cols": n, "nnz": lpa.nnz,
                       "step": "1 HPR iteration (KKT check every 16th)"},
            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
