@@ -218,15 +218,17 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
 #pragma unroll
             for (int w = 0; w < TPB / 32; ++w) t += wpart[w];
             reinterpret_cast<T*>(A.tile_part)[blockIdx.x] = t;
-            __threadfence();
             const int4 lg = A.longs[li];
-            const int prev = atomicAdd(A.counters + li, 1);
+            // release: the partial is visible before the ticket; acquire: the last
+            // CTA sees every partial released before its ticket (no full fences)
+            int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                         : "=r"(prev) : "l"(A.counters + li) : "memory");
             s_last = (prev == lg.z - 1);
         }
         __syncthreads();
         block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
         if (s_last && threadIdx.x == 0) {
-            __threadfence();
             const int4 lg = A.longs[li];
             const volatile T* tp = reinterpret_cast<const volatile T*>(A.tile_part);
             T tot = T(0);
