@@ -226,9 +226,13 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
                          : "=r"(prev) : "l"(A.counters + li) : "memory");
             s_last = (prev == lg.z - 1);
         }
-        __syncthreads();
-        block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
-        if (s_last && threadIdx.x == 0) {
+        if constexpr (Epi::K > 0) {
+            // the partial-sum slots need every thread; without them only thread 0
+            // (which wrote s_last itself) continues, and the other warps retire
+            __syncthreads();
+            block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
+        }
+        if (threadIdx.x == 0 && s_last) {
             const int4 lg = A.longs[li];
             const volatile T* tp = reinterpret_cast<const volatile T*>(A.tile_part);
             T tot = T(0);
