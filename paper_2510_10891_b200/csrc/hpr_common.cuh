@@ -18,7 +18,7 @@ constexpr int TILE_NNZ = 1024;    // nonzeros staged per stream tile (8 KB FP64 
 constexpr int TILE_ROWS = TPB;    // rows per stream tile (one epilogue row per thread)
 constexpr int ITEMS = TILE_NNZ / TPB;
 constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row
-constexpr int MAX_B = 64;         // largest check_every the fused loop body supports
+constexpr int MAX_B = 64;         // largest check_every the loop graph holds (longer: eager blocks)
 
 // quantities accumulated by the two master-space check kernels
 constexpr int KR = 4;   // rows: primal^2, rhs.y, dy^2, nonfinite(bar_y)

@@ -928,6 +928,13 @@ static bool eager_loop() {
     return on || sync_debug();
 }
 
+// the block loop a single-GPU solve runs: the graph holds at most MAX_B
+// iterations per block; a longer check cadence (the reference takes any
+// check_every) runs the same kernels as plain launches, block by block
+static bool use_eager(const hpr_handle* h, long long B) {
+    return !h->comm && (eager_loop() || B > MAX_B);
+}
+
 template <typename T>
 double run_eager(hpr_handle* h, int B) {
     cudaStream_t s = h->stream;
@@ -1005,7 +1012,6 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     h->launches += 3;
 
     const int B = prm->log_every_iteration ? 1 : std::max(1, prm->check_every);
-    if (B > MAX_B) fail(HPR_ERR_INVALID, "check_every too large");
     Ctrl c{};
     c.sigma = sigma;
     c.lam = lam;
@@ -1066,7 +1072,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
                 CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
             }
         }
-        if (eager_loop() && !h->comm) {
+        if (use_eager(h, B)) {
             st->loop_seconds = run_eager<T>(h, B);
         } else {
             ensure_graph<T>(h, p, B);
@@ -1828,7 +1834,7 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
 int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* st) {
     API_BEGIN
     if (!h || !st) fail(HPR_ERR_INVALID, "NULL argument");
-    if (h->last_prec < 0 || (!h->gexec && !eager_loop()))
+    if (h->last_prec < 0 || (!h->gexec && !use_eager(h, h->h_ctrl->B)))
         fail(HPR_ERR_INVALID, "hpr_resume needs a prior looping solve");
     CK(cudaSetDevice(h->dev));
     std::memset(st, 0, sizeof(*st));
@@ -1843,7 +1849,7 @@ int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_sta
     CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     *h->h_ctrl = c;
     if (c.status != -1) st->loop_seconds = 0.0;
-    else if (eager_loop() && !h->comm)
+    else if (use_eager(h, c.B))
         st->loop_seconds = h->last_prec == HPR_FP32 ? run_eager<float>(h, (int)c.B)
                                                     : run_eager<double>(h, (int)c.B);
     else st->loop_seconds = run_loop(h);

@@ -34,6 +34,7 @@ VARIANTS = {
     "bare": dict(tolerance=1e-7, ruiz=False, pock_chambolle=False, check_every=32),
     "iter_limit": dict(tolerance=1e-12, max_iterations=500),
     "tail_only": dict(tolerance=1e-12, max_iterations=10, check_every=16),
+    "long_cadence": dict(tolerance=1e-7, check_every=100, restart_stall=1000),
 }
 KEYS = ("iterations", "restarts", "objective", "lam", "sigma_final")
 
