@@ -344,7 +344,10 @@ class Engine:
         z = np.empty(self.n)
         x0 = y0 = z0 = None
         if start is not None:
-            x0, y0, z0 = (_f64(v) for v in start)
+            # numpy broadcasting as in _ScaleMaps.to_work (hprlp.py:266-270): a
+            # scalar spreads, a wrong length raises ValueError
+            x0, y0, z0 = (_f64(np.broadcast_to(np.asarray(v, dtype=np.float64), (k,)))
+                          for v, k in zip(start, (self.n, self.m, self.n)))
         while True:
             pbuf = _f64(np.concatenate(starts))
             prm = _capi.Params(
@@ -571,7 +574,8 @@ def solve_partitioned(lp, config=None, start=None, comm: NcclComm | None = None,
         eng = Engine(blp, comm=comm)
         sub_start = None
         if start is not None:
-            sub_start = (start[0], np.asarray(start[1])[blk.rows], start[2])
+            y0 = np.broadcast_to(np.asarray(start[1], dtype=np.float64), (csr.shape[0],))
+            sub_start = (start[0], y0[blk.rows], start[2])
         x, yb, z, st, recs = eng.solve_raw(config, sub_start, time.perf_counter() - t_start,
                                            rows=blk.rows, m_total=csr.shape[0])
         parts = [None] * comm.world_size

@@ -176,6 +176,17 @@ def test_limits_and_errors(H):
                             [1.0], [0.0], [2.0], 0)
     with pytest.raises(ValueError):
         H.solve(z)
+    # start vectors follow numpy broadcasting (hprlp.py:266-270): wrong lengths
+    # raise, a scalar spreads over the vector
+    lp, rec, res = golden_io.random_lps()[2]
+    m, n = lp.matrix.csr.shape
+    with pytest.raises(ValueError):
+        H.solve(lp, H.SolverConfig(tolerance=1e-6), start=(np.zeros(n + 1), np.zeros(m),
+                                                            np.zeros(n)))
+    a = H.solve(lp, H.SolverConfig(tolerance=1e-6), start=(0.5, np.zeros(m), 0.0))
+    b = H.solve(lp, H.SolverConfig(tolerance=1e-6), start=(np.full(n, 0.5), np.zeros(m),
+                                                        np.zeros(n)))
+    assert a.iterations == b.iterations and np.array_equal(a.x, b.x)
 
 
 def test_log_every_iteration_rate_log(H):
