@@ -30,7 +30,10 @@ EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_crea
            "hpr_get_layout", "hpr_nccl_unique_id", "hpr_nccl_comm_init",
            "hpr_nccl_comm_destroy",
            # include/hpr_presolve.h (host-only presolve core)
-           "hpr_presolve_run", "hpr_presolve_info", "hpr_presolve_fetch", "hpr_presolve_free")
+           "hpr_presolve_run", "hpr_presolve_info", "hpr_presolve_fetch", "hpr_presolve_free",
+           # include/hpr_screen.h (device flow screen)
+           "hpr_screen_create", "hpr_screen_run", "hpr_screen_fetch", "hpr_screen_flows",
+           "hpr_screen_bench", "hpr_screen_info_get", "hpr_screen_destroy")
 
 _p = C.c_void_p
 
@@ -94,6 +97,12 @@ class Layout(C.Structure):
                 ("index_free_nnz_f", C.c_int64), ("fused", C.c_int32), ("reserved", C.c_int32)]
 
 
+class ScreenInfo(C.Structure):
+    _fields_ = [("n_lines", C.c_int32), ("n_buses", C.c_int32), ("n_tables", C.c_int32),
+                ("bus_pitch", C.c_int32), ("splits", C.c_int32), ("ctas_per_sm", C.c_int32),
+                ("table_bytes", C.c_size_t)]
+
+
 class HprError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"libhprlp_b200 error {code}: {msg}")
@@ -143,6 +152,16 @@ def load(path: str | None = None):
     lib.hpr_presolve_fetch.argtypes = [_p] * 8
     lib.hpr_presolve_free.argtypes = [_p]
     lib.hpr_presolve_free.restype = None
+    lib.hpr_screen_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.POINTER(_p), _p, C.POINTER(_p)]
+    lib.hpr_screen_run.argtypes = [_p, _p, C.c_int32, C.c_double, C.POINTER(C.c_int64)]
+    lib.hpr_screen_fetch.argtypes = [_p] * 6
+    lib.hpr_screen_flows.argtypes = [_p, C.c_int32, _p]
+    lib.hpr_screen_bench.argtypes = [_p, C.c_int32, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)]
+    lib.hpr_screen_info_get.argtypes = [_p, C.POINTER(ScreenInfo)]
+    lib.hpr_screen_destroy.argtypes = [_p]
+    lib.hpr_screen_destroy.restype = None
     _LIB = lib
     return lib
 

@@ -53,6 +53,9 @@ using namespace hpr;
 
 static thread_local std::string g_err;
 
+// shared with hpr_screen.cu so hpr_last_error() reports every entry point
+void hpr_internal_set_error(const char* msg) { g_err = msg; }
+
 struct HprError {
     int code;
 };

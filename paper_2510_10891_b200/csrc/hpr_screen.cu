@@ -1,0 +1,462 @@
+// hpr_screen.cu — the device flow screen behind include/hpr_screen.h.
+//
+// Reference: scuckit.driver.screen_violations (pkg/src/scuckit/driver.py:165-200).
+// Per contingency key it forms flows = PTDF_key (L x B) @ injections (B x T)
+// (driver.py:186) and reports every (line, period) with
+// |flow| - limit > tol * limit (driver.py:187-196).
+//
+// Shape of the work: L x B x T with T = 24..36 periods, so every PTDF element
+// read from HBM feeds T FP64 FMAs: 2T/8 = 9 flop/byte at T = 36, just above
+// B200's FP64-FMA : HBM balance (~37 TF/s : 6.5 TB/s = 5.7 flop/byte).  The
+// product is therefore a register-tiled FP64 FMA kernel (B200's FP64 tensor
+// rate equals its FP64 FMA rate, so DMMA would buy nothing) fed by a
+// three-stage cp.async pipeline:
+//   * a CTA owns 128 lines (4 per lane) and all periods; warp w owns periods
+//     [12w, 12w + 12), so the injection reads are warp-wide broadcasts and a
+//     thread does 48 FMAs per pair of double2 shared loads;
+//   * the PTDF tile rows sit at a pitch of 18 doubles, so the lanes' double2
+//     reads hit distinct banks (8 lanes per 128-byte wavefront);
+//   * the bus range is split S ways (grid.y) so that row tiles x S fill whole
+//     waves of resident CTAs; the S partial sums are added in split order by
+//     the epilogue kernel, which also applies the threshold test and compacts
+//     the violations (deterministic flows; the record order is not, and the
+//     host sorts with the reference's key).
+// The tables stay resident (PtdfTable is immutable, instance.py:141-164),
+// padded to a bus pitch that is a multiple of 16 with zero columns.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "../../include/hpr_screen.h"
+#include "../../include/hprlp_b200.h"
+
+void hpr_internal_set_error(const char* msg);  // hpr_engine.cu (hpr_last_error)
+
+namespace {
+
+constexpr int RT = 4;             // lines per lane
+constexpr int ROWS = 32 * RT;     // lines per CTA
+constexpr int TPW = 12;           // periods per warp
+constexpr int MAXW = 8;           // warps per CTA -> at most 96 periods
+constexpr int KB = 16;            // buses per pipeline stage
+constexpr int PP = KB + 2;        // shared pitch of a PTDF row (doubles)
+constexpr int STAGES = 3;
+
+struct ScreenErr {
+    int code;
+};
+
+void fail(int code, const std::string& msg) {
+    hpr_internal_set_error(msg.c_str());
+    throw ScreenErr{code};
+}
+
+#define SCK(call)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            fail(HPR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+size_t product_smem(int w) { return (size_t)STAGES * (ROWS * PP + KB * w * TPW) * sizeof(double); }
+
+// part[(split * NT + table) * L * Tp + line * Tp + t] = sum over the split's
+// buses of PTDF[table][line][b] * inj[b][t]   (b ascending within the split)
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+screen_product(const double* __restrict__ tab, const double* __restrict__ inj,
+               double* __restrict__ part, int L, int Bp, int NT, int kper) {
+    constexpr int TP = W * TPW;
+    constexpr int NTHR = W * 32;
+    extern __shared__ __align__(16) double sm[];
+    double* Ps = sm;                          // STAGES x ROWS x PP
+    double* Is = sm + STAGES * ROWS * PP;     // STAGES x KB x TP
+
+    const int tb = blockIdx.z, split = blockIdx.y;
+    const int row0 = blockIdx.x * ROWS;
+    const double* T0 = tab + (size_t)tb * L * Bp;
+    const int k0 = split * kper;
+    const int nk = min(kper, Bp - k0) / KB;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    auto load = [&](int stage, int kt) {
+        const int kb = k0 + kt * KB;
+        double* ps = Ps + stage * ROWS * PP;
+#pragma unroll 4
+        for (int c = tid; c < ROWS * (KB / 2); c += NTHR) {
+            const int r = c / (KB / 2), q = c % (KB / 2);
+            const int gr = min(row0 + r, L - 1);
+            cp_async16(ps + r * PP + 2 * q, T0 + (size_t)gr * Bp + kb + 2 * q);
+        }
+        double* is = Is + stage * KB * TP;
+        const double* src = inj + (size_t)kb * TP;
+        for (int c = tid; c < KB * TP / 2; c += NTHR) cp_async16(is + 2 * c, src + 2 * c);
+        cp_async_commit();
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load(s, s);
+        else cp_async_commit();
+    }
+
+    double acc[RT][TPW];
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) acc[i][j] = 0.0;
+
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        const int nx = kt + STAGES - 1;
+        if (nx < nk) load(nx % STAGES, nx);
+        else cp_async_commit();
+        const double* ps = Ps + (kt % STAGES) * ROWS * PP;
+        const double* is = Is + (kt % STAGES) * KB * TP + w * TPW;
+#pragma unroll
+        for (int kk = 0; kk < KB; kk += 2) {
+            double2 p[RT];
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+                p[i] = *reinterpret_cast<const double2*>(ps + (lane + 32 * i) * PP + kk);
+#pragma unroll
+            for (int j = 0; j < TPW; j += 2) {
+                const double2 a = *reinterpret_cast<const double2*>(is + kk * TP + j);
+                const double2 b = *reinterpret_cast<const double2*>(is + (kk + 1) * TP + j);
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    acc[i][j] = __fma_rn(p[i].x, a.x, acc[i][j]);
+                    acc[i][j + 1] = __fma_rn(p[i].x, a.y, acc[i][j + 1]);
+                    acc[i][j] = __fma_rn(p[i].y, b.x, acc[i][j]);
+                    acc[i][j + 1] = __fma_rn(p[i].y, b.y, acc[i][j + 1]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+
+    double* out = part + ((size_t)split * NT + tb) * L * TP;
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+        const int row = row0 + lane + 32 * i;
+        if (row < L) {
+#pragma unroll
+            for (int j = 0; j < TPW; j += 2)
+                *reinterpret_cast<double2*>(out + (size_t)row * TP + w * TPW + j) =
+                    make_double2(acc[i][j], acc[i][j + 1]);
+        }
+    }
+}
+
+// flows = sum of the S partials in split order; the reference's test
+// excess = |flow| - limit > tol * limit (driver.py:190-191; NaN never passes).
+__global__ void screen_epilogue(const double* __restrict__ part, const double* __restrict__ lim,
+                                double* __restrict__ flows, int NT, int L, int T, int Tp, int S,
+                                double tol, unsigned long long* cnt, long long cap,
+                                int* r_tab, int* r_line, int* r_per, double* r_flow,
+                                double* r_exc) {
+    const long long total = (long long)NT * L * T;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(idx % T);
+        const long long lt = idx / T;
+        const int l = (int)(lt % L), tb = (int)(lt / L);
+        double f = 0.0;
+        for (int s = 0; s < S; ++s) f += part[((size_t)s * NT + tb) * L * Tp + (size_t)l * Tp + t];
+        flows[idx] = f;
+        const double limit = lim[(size_t)tb * L + l];
+        const double ex = fabs(f) - limit;
+        if (ex > tol * limit) {
+            const unsigned long long k = atomicAdd(cnt, 1ULL);
+            if ((long long)k < cap) {
+                r_tab[k] = tb;
+                r_line[k] = l;
+                r_per[k] = t;
+                r_flow[k] = f;
+                r_exc[k] = ex;
+            }
+        }
+    }
+}
+
+template <int W>
+void launch_product(dim3 grid, cudaStream_t s, const double* tab, const double* inj, double* part,
+                    int L, int Bp, int NT, int kper) {
+    screen_product<W><<<grid, W * 32, product_smem(W), s>>>(tab, inj, part, L, Bp, NT, kper);
+}
+
+using ProductFn = void (*)(dim3, cudaStream_t, const double*, const double*, double*, int, int,
+                           int, int);
+const ProductFn kProducts[MAXW] = {launch_product<1>, launch_product<2>, launch_product<3>,
+                                   launch_product<4>, launch_product<5>, launch_product<6>,
+                                   launch_product<7>, launch_product<8>};
+const void* kProductFns[MAXW] = {(const void*)screen_product<1>, (const void*)screen_product<2>,
+                                 (const void*)screen_product<3>, (const void*)screen_product<4>,
+                                 (const void*)screen_product<5>, (const void*)screen_product<6>,
+                                 (const void*)screen_product<7>, (const void*)screen_product<8>};
+
+template <typename T> void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+}  // namespace
+
+struct hpr_screen {
+    int dev = 0, L = 0, B = 0, NT = 0, Bp = 0, sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    double* tab = nullptr;   // NT x L x Bp
+    double* lim = nullptr;   // NT x L
+    // per-run state (sized for the largest T seen)
+    int T = 0, W = 0, Tp = 0, S = 1, kper = 0, ctas = 0;
+    double tol = 0.0;
+    long long cap = 0, found = 0;
+    double* inj = nullptr;   // Bp x Tp, zero padded
+    double* part = nullptr;  // S x NT x L x Tp
+    double* flows = nullptr; // NT x L x T
+    size_t inj_cap = 0, part_cap = 0, flows_cap = 0;
+    unsigned long long* cnt = nullptr;
+    int *r_tab = nullptr, *r_line = nullptr, *r_per = nullptr;
+    double *r_flow = nullptr, *r_exc = nullptr;
+
+    ~hpr_screen() {
+        if (stream) cudaStreamSynchronize(stream);
+        dfree(tab); dfree(lim); dfree(inj); dfree(part); dfree(flows); dfree(cnt);
+        dfree(r_tab); dfree(r_line); dfree(r_per); dfree(r_flow); dfree(r_exc);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    template <typename T> void grow(T*& p, size_t& have, size_t need) {
+        if (need <= have) return;
+        dfree(p);
+        SCK(cudaMalloc(&p, need * sizeof(T)));
+        have = need;
+    }
+
+    // bus splits: row tiles x S x NT should fill whole waves of resident CTAs
+    void plan() {
+        int per_sm = 0;
+        SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kProductFns[W - 1], W * 32,
+                                                          product_smem(W)));
+        if (per_sm < 1) fail(HPR_ERR_CUDA, "screen product kernel does not fit on an SM");
+        ctas = per_sm;
+        const long long resident = (long long)per_sm * sms;
+        const long long row_tiles = (long long)(L + ROWS - 1) / ROWS * NT;
+        const int stages = Bp / KB;
+        const int s_max = std::max(1, std::min(32, stages / 8));  // >= 128 buses per split
+        int best = 1;
+        double best_eff = 0.0;
+        for (int s = 1; s <= s_max; ++s) {
+            const int kp = (stages + s - 1) / s;
+            const int se = (stages + kp - 1) / kp;
+            const long long tiles = row_tiles * se;
+            const long long waves = (tiles + resident - 1) / resident;
+            const double eff = (double)tiles / (double)(waves * resident);
+            if (eff > best_eff + 0.05) {
+                best_eff = eff;
+                best = s;
+            }
+            if (eff >= 0.9) break;
+        }
+        const int kp = (stages + best - 1) / best;
+        kper = kp * KB;
+        S = (stages + kp - 1) / kp;
+    }
+
+    void launch() {
+        dim3 grid((L + ROWS - 1) / ROWS, S, NT);
+        kProducts[W - 1](grid, stream, tab, inj, part, L, Bp, NT, kper);
+        SCK(cudaGetLastError());
+    }
+    void epilogue() {
+        SCK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), stream));
+        const long long total = (long long)NT * L * T;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 16);
+        screen_epilogue<<<std::max(blocks, 1), 256, 0, stream>>>(
+            part, lim, flows, NT, L, T, Tp, S, tol, cnt, cap, r_tab, r_line, r_per, r_flow, r_exc);
+        SCK(cudaGetLastError());
+    }
+};
+
+#define SCREEN_API_BEGIN try {
+#define SCREEN_API_END                                                                   \
+    }                                                                                    \
+    catch (const ScreenErr& e) {                                                         \
+        return e.code;                                                                   \
+    }                                                                                    \
+    catch (const std::exception& e) {                                                    \
+        hpr_internal_set_error(e.what());                                                \
+        return HPR_ERR_NOMEM;                                                            \
+    }                                                                                    \
+    return 0;
+
+extern "C" int hpr_screen_create(int32_t device, int32_t n_lines, int32_t n_buses,
+                                 int32_t n_tables, const double* const* tables,
+                                 const double* limits, hpr_screen** out) {
+    SCREEN_API_BEGIN
+    if (!out || !tables || !limits) fail(HPR_ERR_INVALID, "hpr_screen_create: null argument");
+    *out = nullptr;
+    if (n_lines <= 0 || n_buses <= 0 || n_tables <= 0)
+        fail(HPR_ERR_EMPTY, "hpr_screen_create: empty PTDF table set");
+    SCK(cudaSetDevice(device));
+    auto* h = new hpr_screen();
+    try {
+        h->dev = device;
+        h->L = n_lines;
+        h->B = n_buses;
+        h->NT = n_tables;
+        h->Bp = (n_buses + KB - 1) / KB * KB;
+        SCK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+        SCK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        for (auto& e : h->ev) SCK(cudaEventCreate(&e));
+        for (int w = 1; w <= MAXW; ++w)
+            SCK(cudaFuncSetAttribute(kProductFns[w - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)product_smem(w)));
+        const size_t per = (size_t)h->L * h->Bp;
+        SCK(cudaMalloc(&h->tab, per * h->NT * sizeof(double)));
+        SCK(cudaMalloc(&h->lim, (size_t)h->L * h->NT * sizeof(double)));
+        SCK(cudaMemsetAsync(h->tab, 0, per * h->NT * sizeof(double), h->stream));
+        for (int k = 0; k < n_tables; ++k) {
+            if (!tables[k]) fail(HPR_ERR_INVALID, "hpr_screen_create: null table");
+            SCK(cudaMemcpy2DAsync(h->tab + per * k, (size_t)h->Bp * sizeof(double), tables[k],
+                                  (size_t)h->B * sizeof(double), (size_t)h->B * sizeof(double),
+                                  h->L, cudaMemcpyDefault, h->stream));
+        }
+        SCK(cudaMemcpyAsync(h->lim, limits, (size_t)h->L * h->NT * sizeof(double),
+                            cudaMemcpyDefault, h->stream));
+        SCK(cudaMalloc(&h->cnt, sizeof(unsigned long long)));
+        SCK(cudaStreamSynchronize(h->stream));
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    SCREEN_API_END
+}
+
+extern "C" int hpr_screen_run(hpr_screen* h, const double* injections, int32_t n_periods,
+                              double tol, int64_t* n_found) {
+    SCREEN_API_BEGIN
+    if (!h || !injections || !n_found) fail(HPR_ERR_INVALID, "hpr_screen_run: null argument");
+    if (n_periods <= 0) fail(HPR_ERR_EMPTY, "hpr_screen_run: no periods");
+    if (n_periods > MAXW * TPW)
+        fail(HPR_ERR_INVALID, "hpr_screen_run: more than 96 periods per screen");
+    SCK(cudaSetDevice(h->dev));
+    h->T = n_periods;
+    h->W = (n_periods + TPW - 1) / TPW;
+    h->Tp = h->W * TPW;
+    h->tol = tol;
+    h->plan();
+    h->grow(h->inj, h->inj_cap, (size_t)h->Bp * h->Tp);
+    h->grow(h->part, h->part_cap, (size_t)h->S * h->NT * h->L * h->Tp);
+    const size_t n_out = (size_t)h->NT * h->L * h->T;
+    if ((long long)n_out > h->cap) {
+        dfree(h->r_tab); dfree(h->r_line); dfree(h->r_per); dfree(h->r_flow); dfree(h->r_exc);
+        SCK(cudaMalloc(&h->r_tab, n_out * sizeof(int)));
+        SCK(cudaMalloc(&h->r_line, n_out * sizeof(int)));
+        SCK(cudaMalloc(&h->r_per, n_out * sizeof(int)));
+        SCK(cudaMalloc(&h->r_flow, n_out * sizeof(double)));
+        SCK(cudaMalloc(&h->r_exc, n_out * sizeof(double)));
+        h->cap = (long long)n_out;
+    }
+    h->grow(h->flows, h->flows_cap, n_out);
+    SCK(cudaMemsetAsync(h->inj, 0, (size_t)h->Bp * h->Tp * sizeof(double), h->stream));
+    SCK(cudaMemcpy2DAsync(h->inj, (size_t)h->Tp * sizeof(double), injections,
+                          (size_t)h->T * sizeof(double), (size_t)h->T * sizeof(double), h->B,
+                          cudaMemcpyDefault, h->stream));
+    h->launch();
+    h->epilogue();
+    unsigned long long c = 0;
+    SCK(cudaMemcpyAsync(&c, h->cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+    SCK(cudaStreamSynchronize(h->stream));
+    h->found = (long long)c;
+    *n_found = (int64_t)c;
+    SCREEN_API_END
+}
+
+extern "C" int hpr_screen_fetch(hpr_screen* h, int32_t* table, int32_t* line, int32_t* period,
+                                double* flow, double* excess) {
+    SCREEN_API_BEGIN
+    if (!h) fail(HPR_ERR_INVALID, "hpr_screen_fetch: null handle");
+    SCK(cudaSetDevice(h->dev));
+    const size_t n = (size_t)h->found;
+    if (n) {
+        if (table) SCK(cudaMemcpyAsync(table, h->r_tab, n * 4, cudaMemcpyDefault, h->stream));
+        if (line) SCK(cudaMemcpyAsync(line, h->r_line, n * 4, cudaMemcpyDefault, h->stream));
+        if (period) SCK(cudaMemcpyAsync(period, h->r_per, n * 4, cudaMemcpyDefault, h->stream));
+        if (flow) SCK(cudaMemcpyAsync(flow, h->r_flow, n * 8, cudaMemcpyDefault, h->stream));
+        if (excess) SCK(cudaMemcpyAsync(excess, h->r_exc, n * 8, cudaMemcpyDefault, h->stream));
+    }
+    SCK(cudaStreamSynchronize(h->stream));
+    SCREEN_API_END
+}
+
+extern "C" int hpr_screen_flows(hpr_screen* h, int32_t table, double* flows) {
+    SCREEN_API_BEGIN
+    if (!h || !flows) fail(HPR_ERR_INVALID, "hpr_screen_flows: null argument");
+    if (h->T == 0) fail(HPR_ERR_INVALID, "hpr_screen_flows: no screen has run");
+    if (table < 0 || table >= h->NT) fail(HPR_ERR_INVALID, "hpr_screen_flows: table out of range");
+    SCK(cudaSetDevice(h->dev));
+    const size_t per = (size_t)h->L * h->T;
+    SCK(cudaMemcpyAsync(flows, h->flows + per * table, per * sizeof(double), cudaMemcpyDefault,
+                        h->stream));
+    SCK(cudaStreamSynchronize(h->stream));
+    SCREEN_API_END
+}
+
+extern "C" int hpr_screen_bench(hpr_screen* h, int32_t reps, double* us_product,
+                                double* us_epilogue) {
+    SCREEN_API_BEGIN
+    if (!h || reps <= 0) fail(HPR_ERR_INVALID, "hpr_screen_bench: bad argument");
+    if (h->T == 0) fail(HPR_ERR_INVALID, "hpr_screen_bench: no screen has run");
+    SCK(cudaSetDevice(h->dev));
+    h->launch();  // warm
+    h->epilogue();
+    SCK(cudaEventRecord(h->ev[0], h->stream));
+    for (int r = 0; r < reps; ++r) h->launch();
+    SCK(cudaEventRecord(h->ev[1], h->stream));
+    for (int r = 0; r < reps; ++r) h->epilogue();
+    SCK(cudaEventRecord(h->ev[2], h->stream));
+    SCK(cudaEventSynchronize(h->ev[2]));
+    float a = 0, b = 0;
+    SCK(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+    SCK(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+    if (us_product) *us_product = 1e3 * a / reps;
+    if (us_epilogue) *us_epilogue = 1e3 * b / reps;
+    SCREEN_API_END
+}
+
+extern "C" int hpr_screen_info_get(hpr_screen* h, hpr_screen_info* info) {
+    SCREEN_API_BEGIN
+    if (!h || !info) fail(HPR_ERR_INVALID, "hpr_screen_info_get: null argument");
+    info->n_lines = h->L;
+    info->n_buses = h->B;
+    info->n_tables = h->NT;
+    info->bus_pitch = h->Bp;
+    info->splits = h->S;
+    info->ctas_per_sm = h->ctas;
+    info->table_bytes = (size_t)h->NT * h->L * h->Bp * sizeof(double);
+    SCREEN_API_END
+}
+
+extern "C" void hpr_screen_destroy(hpr_screen* h) {
+    if (!h) return;
+    cudaSetDevice(h->dev);
+    delete h;
+}

@@ -616,7 +616,10 @@ _SAVED = {}
 _PRESOLVE_SITES = ("scuckit.presolve", "scuckit.fixing", "scuckit.milp_bb", "scuckit")
 
 
-def install(module=None, presolve: bool = True):
+_SCREEN_SITES = ("scuckit.driver", "scuckit")
+
+
+def install(module=None, presolve: bool = True, screen: bool = True):
     """Route the reference's LP solves to the GPU engine.
 
     Rebinds ``scuckit.hprlp.solve`` (and ``kkt_residual`` / ``hpr_iterate``)
@@ -624,7 +627,10 @@ def install(module=None, presolve: bool = True):
     ``presolve`` the reference's ``milp_presolve`` / ``lp_presolve`` are
     rebound too, in every module that imported them by name (presolve.py,
     fixing.py:22, milp_bb.py:26, the package namespace), to the native-core
-    mirror in ``paper_2510_10891_b200.presolve`` (bit-identical reductions)."""
+    mirror in ``paper_2510_10891_b200.presolve`` (bit-identical reductions).
+    With ``screen`` the driver's post-MILP flow screen
+    (``driver.screen_violations``, ``driver.py:165-200``, called by name at
+    ``:288``) is rebound to the device screen in ``screen.py``."""
     import importlib
     if module is None:
         import scuckit.hprlp as module
@@ -649,6 +655,15 @@ def install(module=None, presolve: bool = True):
                 if hasattr(mod, fn):
                     _SAVED["presolve"].setdefault((name, fn), getattr(mod, fn))
                     setattr(mod, fn, getattr(native, fn))
+    if screen:
+        from . import screen as dev_screen
+        drv = importlib.import_module("scuckit.driver")
+        dev_screen._VIOLATION_CLASS = drv.Violation
+        for name in _SCREEN_SITES:
+            mod = importlib.import_module(name)
+            if hasattr(mod, "screen_violations"):
+                _SAVED.setdefault("screen", {}).setdefault(name, mod.screen_violations)
+                mod.screen_violations = dev_screen.screen_violations
     return module
 
 
@@ -662,8 +677,12 @@ def uninstall():
     module.hpr_iterate = _SAVED["hpr_iterate"]
     for (name, fn), orig in _SAVED.get("presolve", {}).items():
         setattr(importlib.import_module(name), fn, orig)
+    for name, orig in _SAVED.get("screen", {}).items():
+        importlib.import_module(name).screen_violations = orig
     from . import presolve as native
     native._LOG_CLASS = native.ReductionLog
+    from . import screen as dev_screen
+    dev_screen._VIOLATION_CLASS = dev_screen.Violation
     _CLS.status, _CLS.result, _CLS.kkt, _CLS.precision = (SolveStatus, SolveResult,
                                                           KktResidual, Precision)
     _SAVED.clear()

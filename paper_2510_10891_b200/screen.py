@@ -1,0 +1,193 @@
+"""Device flow screen: mirror of ``scuckit.driver.screen_violations``.
+
+Reference: ``pkg/src/scuckit/driver.py:165-200``.  After each MILP pass the
+driver checks the unscaled point against every (line, period, contingency):
+net injections per bus and period are rebuilt from the point
+(``driver.py:176-181``), flows are ``ptdf.table(key) @ injections`` for every
+key (``:185-186``) and a triple is reported when
+``|flow| - limit > tol * limit`` (``:187-196``), sorted by excess, largest
+first (``:199``).
+
+Here the injections are rebuilt on the host exactly as the reference builds
+them (same numpy operations in the same order, so bit-identical), and the
+products plus the threshold test run on the GPU (``csrc/hpr_screen.cu``,
+C-ABI ``include/hpr_screen.h``) against PTDF tables that stay resident in HBM
+for the lifetime of the (immutable) ``PtdfTable``.  The FP64 sums are taken
+in a different order than the host BLAS, so flows agree to rounding
+(~1e-15 relative), and the violation set is the reference's except for
+entries within rounding of the threshold.
+
+There is no CPU fallback: without the library or a CUDA device the first
+screen raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+
+
+@dataclass
+class Violation:
+    """Mirror of ``scuckit.driver.Violation`` (``driver.py:68-81``);
+    ``install()`` switches results to the reference's own class."""
+    line: str
+    period: int
+    contingency: str
+    flow: float
+    limit: float
+    excess: float
+    already_monitored: bool = False
+
+    @property
+    def triple(self) -> tuple:
+        return (self.line, self.period, self.contingency)
+
+
+_VIOLATION_CLASS = Violation
+
+
+def column_blocks(instance):
+    """The columns ``screen_violations`` reads, as ``VariableMap`` lays them
+    out (``formulation.py:42-70``): u at 0, p' at 3GT, then the segment
+    columns (T * H_g per unit), the cost block (GT) and the unserved-demand
+    block (B x T).  Returns (u, pprime, penalty, n_cols)."""
+    n_g = len(instance.generators)
+    n_t = instance.n_periods
+    n_b = len(instance.buses)
+    gt = n_g * n_t
+    u = np.arange(gt, dtype=np.int64).reshape(n_g, n_t)
+    pprime = 3 * gt + u
+    col = 4 * gt + n_t * sum(g.n_segments for g in instance.generators) + gt
+    penalty = col + np.arange(n_b * n_t, dtype=np.int64).reshape(n_b, n_t)
+    return u, pprime, penalty, col + n_b * n_t
+
+
+def injections(point, instance) -> np.ndarray:
+    """Net injections (n_buses x n_periods), ``driver.py:176-181``."""
+    u, pprime, penalty, n_cols = column_blocks(instance)
+    point = np.asarray(point, dtype=np.float64)
+    if point.shape[0] != n_cols:
+        raise ValueError("point length does not match the instance's model")
+    demand = instance.demand_matrix()
+    bus_idx = instance.network.bus_index()
+    power = point[pprime] + np.array([[g.p_min] for g in instance.generators]) * point[u]
+    inj = -(demand - point[penalty])
+    rows = np.array([bus_idx[g.bus] for g in instance.generators], dtype=np.int64)
+    # unbuffered, in generator order: the same sequence of adds as the
+    # reference's per-generator loop (driver.py:180-181)
+    np.add.at(inj, rows, power)
+    return inj
+
+
+class FlowScreen:
+    """PTDF tables of one ``PtdfTable`` resident on one GPU, with the per-key
+    line limits (``Line.limit_for``, ``instance.py:88-89``)."""
+
+    def __init__(self, ptdf, keys, lines, device: int = 0):
+        self.lib = _capi.load()
+        self.keys = list(keys)
+        self.line_ids = [ln.lid for ln in lines]
+        tabs = [np.ascontiguousarray(ptdf.table(k), dtype=np.float64) for k in self.keys]
+        n_l, n_b = tabs[0].shape
+        if n_l != len(self.line_ids):
+            raise ValueError("PTDF rows do not match the instance's lines")
+        self.limits = np.ascontiguousarray(
+            [[ln.limit_for(k) for ln in lines] for k in self.keys], dtype=np.float64)
+        self.shape = (n_l, n_b)
+        self._last_t = 0
+        ptrs = (C.c_void_p * len(tabs))(*[t.ctypes.data for t in tabs])
+        h = C.c_void_p()
+        _capi.check(self.lib.hpr_screen_create(device, n_l, n_b, len(tabs), ptrs,
+                                               _capi.ptr(self.limits), C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, self.lib.hpr_screen_destroy, h)
+
+    def close(self):
+        self._fin()
+
+    def info(self) -> dict:
+        info = _capi.ScreenInfo()
+        _capi.check(self.lib.hpr_screen_info_get(self.handle, C.byref(info)))
+        return {k: getattr(info, k) for k, _ in info._fields_}
+
+    def run(self, inj: np.ndarray, tol: float):
+        """Screen an (n_buses x n_periods) injection matrix; returns the
+        records (table, line, period, flow, excess) as numpy arrays."""
+        inj = np.ascontiguousarray(inj, dtype=np.float64)
+        if inj.ndim != 2 or inj.shape[0] != self.shape[1]:
+            raise ValueError("injections must be (n_buses, n_periods)")
+        n = C.c_int64()
+        _capi.check(self.lib.hpr_screen_run(self.handle, _capi.ptr(inj), inj.shape[1],
+                                            float(tol), C.byref(n)))
+        self._last_t = inj.shape[1]
+        k = n.value
+        rec = (np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k, np.int32),
+               np.empty(k, np.float64), np.empty(k, np.float64))
+        _capi.check(self.lib.hpr_screen_fetch(self.handle, *[_capi.ptr(a) for a in rec]))
+        return rec
+
+    def flows(self, table: int = 0) -> np.ndarray:
+        """Flows of one table from the last run (``PtdfTable.flows``,
+        ``instance.py:170-173``)."""
+        out = np.empty((self.shape[0], self._last_t), np.float64)
+        _capi.check(self.lib.hpr_screen_flows(self.handle, table, _capi.ptr(out)))
+        return out
+
+    def bench(self, reps: int = 20) -> tuple:
+        a, b = C.c_double(), C.c_double()
+        _capi.check(self.lib.hpr_screen_bench(self.handle, reps, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+_SCREENS: dict = {}
+
+
+def screen_for(ptdf, instance, device: int = 0) -> FlowScreen:
+    """The resident screen of ``ptdf`` (built once; ``PtdfTable`` is
+    immutable, ``instance.py:141-147``), rebuilt only if the instance's keys
+    or limits differ from the ones it was built with."""
+    keys = instance.contingency_keys()
+    ent = _SCREENS.get(id(ptdf))
+    if ent is not None:
+        ref, scr = ent
+        if ref() is ptdf and scr.keys == keys and scr.line_ids == [ln.lid for ln in instance.lines]:
+            lim = np.array([[ln.limit_for(k) for ln in instance.lines] for k in keys])
+            if np.array_equal(lim, scr.limits):
+                return scr
+        scr.close()
+    scr = FlowScreen(ptdf, keys, instance.lines, device=device)
+    try:
+        ref = weakref.ref(ptdf, lambda _r, key=id(ptdf): _drop(key))
+    except TypeError:  # not weak-referenceable: keep it alive with the cache entry
+        ref = (lambda obj: (lambda: obj))(ptdf)
+    _SCREENS[id(ptdf)] = (ref, scr)
+    return scr
+
+
+def _drop(key):
+    ent = _SCREENS.pop(key, None)
+    if ent is not None:
+        ent[1].close()
+
+
+def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) -> list:
+    """Flow check of a primal vector over every (line, period, contingency);
+    same signature, errors and result order as ``driver.py:165-200``."""
+    inj = injections(point, instance)
+    monitored = set(monitored)
+    scr = screen_for(ptdf, instance)
+    tab, line, per, flow, exc = scr.run(inj, tol)
+    keys, lids, lim = scr.keys, scr.line_ids, scr.limits
+    out = [_VIOLATION_CLASS(line=lids[l], period=int(t), contingency=keys[k], flow=float(f),
+                            limit=float(lim[k, l]), excess=float(e),
+                            already_monitored=(lids[l], int(t), keys[k]) in monitored)
+           for k, l, t, f, e in zip(tab.tolist(), line.tolist(), per.tolist(), flow.tolist(),
+                                    exc.tolist())]
+    out.sort(key=lambda v: (-v.excess, v.line, v.period, v.contingency))
+    return out
