@@ -6,21 +6,24 @@
 // |flow| - limit > tol * limit (driver.py:187-196).
 //
 // Shape of the work: L x B x T with T = 24..36 periods, so every PTDF element
-// read from HBM feeds T FP64 FMAs: 2T/8 = 9 flop/byte at T = 36, just above
-// B200's FP64-FMA : HBM balance (~37 TF/s : 6.5 TB/s = 5.7 flop/byte).  The
-// product is therefore a register-tiled FP64 FMA kernel (B200's FP64 tensor
-// rate equals its FP64 FMA rate, so DMMA would buy nothing) fed by a
-// three-stage cp.async pipeline:
-//   * a CTA owns 128 lines (4 per lane) and all periods; warp w owns periods
-//     [12w, 12w + 12), so the injection reads are warp-wide broadcasts and a
-//     thread does 48 FMAs per pair of double2 shared loads;
-//   * the PTDF tile rows sit at a pitch of 18 doubles, so the lanes' double2
-//     reads hit distinct banks (8 lanes per 128-byte wavefront);
-//   * the bus range is split S ways (grid.y) so that row tiles x S fill whole
-//     waves of resident CTAs; the S partial sums are added in split order by
-//     the epilogue kernel, which also applies the threshold test and compacts
-//     the violations (deterministic flows; the record order is not, and the
-//     host sorts with the reference's key).
+// read from HBM feeds T FP64 multiply-adds: 2T/8 = 9 flop/byte at T = 36, above
+// the FP64 : HBM balance of this chip (~33 TF/s DMMA measured : 6.5 TB/s), so
+// the product is bound by FP64 math, not HBM.  It runs on the FP64 tensor
+// pipe (mma.sync m8n8k4 .f64, DMMA) fed by a three-stage cp.async pipeline:
+//   * a CTA owns 128 lines; warp (wm, wn) owns lines [32 wm, 32 wm + 32) as
+//     four 8-line m-tiles and NTW 8-period n-tiles (a second warp row wn = 1
+//     only when T > 48);
+//   * A fragments (8 lines x 4 buses) are read from the staged PTDF tile at a
+//     pitch of 20 doubles, B fragments (4 buses x 8 periods) from the staged
+//     injection tile: both at the two-wavefront minimum per warp load;
+//   * the bus range is split S ways (grid.y), S chosen so row tiles x S fill
+//     whole waves of resident CTAs; the S partial sums are added in split
+//     order by the epilogue kernel, which also applies the threshold test and
+//     compacts the violations (deterministic flows; the record order is not,
+//     and the host sorts with the reference's key).
+// A/B on one B200 at C4 (20,467 x 13,659 x 36): register-tiled DFMA kernel
+// (4 lines x 12 periods per thread, broadcast injection reads) 1,243 us,
+// FP64 pipe 49% busy; this DMMA kernel 808 us, tensor pipe 84% busy (ncu).
 // The tables stay resident (PtdfTable is immutable, instance.py:141-164),
 // padded to a bus pitch that is a multiple of 16 with zero columns.
 
@@ -37,12 +40,8 @@ void hpr_internal_set_error(const char* msg);  // hpr_engine.cu (hpr_last_error)
 
 namespace {
 
-constexpr int RT = 4;             // lines per lane
-constexpr int ROWS = 32 * RT;     // lines per CTA
-constexpr int TPW = 12;           // periods per warp
-constexpr int MAXW = 8;           // warps per CTA -> at most 96 periods
+constexpr int ROWS = 128;         // lines per CTA (4 warps x 32)
 constexpr int KB = 16;            // buses per pipeline stage
-constexpr int PP = KB + 2;        // shared pitch of a PTDF row (doubles)
 constexpr int STAGES = 3;
 
 struct ScreenErr {
@@ -70,35 +69,50 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-size_t product_smem(int w) { return (size_t)STAGES * (ROWS * PP + KB * w * TPW) * sizeof(double); }
+// Tensor-core form (DMMA, mma.sync m8n8k4 FP64): a warp owns 32 lines (4 m-tiles)
+// x NTW period tiles of 8; four warps cover the CTA's 128 lines, and a second
+// warp row takes period tiles NTW.. when T > 8 * NTW.  Fragments come straight
+// from the staged tiles: A (8 lines x 4 buses) at a pitch of 20 doubles and
+// B (4 buses x 8 periods) from the injection tile, both at the minimum two
+// wavefronts per load.
+constexpr int MPP = KB + 4;
+constexpr int NTW_MAX = 6;
+size_t mma_smem(int ntw, int wn) {
+    return (size_t)STAGES * (ROWS * MPP + KB * wn * ntw * 8) * sizeof(double);
+}
 
-// part[(split * NT + table) * L * Tp + line * Tp + t] = sum over the split's
-// buses of PTDF[table][line][b] * inj[b][t]   (b ascending within the split)
-template <int W>
-__global__ void __launch_bounds__(W * 32)
-screen_product(const double* __restrict__ tab, const double* __restrict__ inj,
-               double* __restrict__ part, int L, int Bp, int NT, int kper) {
-    constexpr int TP = W * TPW;
-    constexpr int NTHR = W * 32;
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int NTW>
+__global__ void __launch_bounds__(256)
+screen_product_mma(const double* __restrict__ tab, const double* __restrict__ inj,
+                   double* __restrict__ part, int L, int Bp, int NT, int kper, int wn_count) {
+    const int TP = wn_count * NTW * 8;
+    const int NTHR = blockDim.x;
     extern __shared__ __align__(16) double sm[];
-    double* Ps = sm;                          // STAGES x ROWS x PP
-    double* Is = sm + STAGES * ROWS * PP;     // STAGES x KB x TP
+    double* Ps = sm;                          // STAGES x ROWS x MPP
+    double* Is = sm + STAGES * ROWS * MPP;    // STAGES x KB x TP
 
     const int tb = blockIdx.z, split = blockIdx.y;
     const int row0 = blockIdx.x * ROWS;
     const double* T0 = tab + (size_t)tb * L * Bp;
     const int k0 = split * kper;
     const int nk = min(kper, Bp - k0) / KB;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, tq = lane & 3;
 
     auto load = [&](int stage, int kt) {
         const int kb = k0 + kt * KB;
-        double* ps = Ps + stage * ROWS * PP;
+        double* ps = Ps + stage * ROWS * MPP;
 #pragma unroll 4
         for (int c = tid; c < ROWS * (KB / 2); c += NTHR) {
             const int r = c / (KB / 2), q = c % (KB / 2);
             const int gr = min(row0 + r, L - 1);
-            cp_async16(ps + r * PP + 2 * q, T0 + (size_t)gr * Bp + kb + 2 * q);
+            cp_async16(ps + r * MPP + 2 * q, T0 + (size_t)gr * Bp + kb + 2 * q);
         }
         double* is = Is + stage * KB * TP;
         const double* src = inj + (size_t)kb * TP;
@@ -112,11 +126,11 @@ screen_product(const double* __restrict__ tab, const double* __restrict__ inj,
         else cp_async_commit();
     }
 
-    double acc[RT][TPW];
+    double acc[4][NTW][2];
 #pragma unroll
-    for (int i = 0; i < RT; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < TPW; ++j) acc[i][j] = 0.0;
+        for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int kt = 0; kt < nk; ++kt) {
         cp_async_wait<STAGES - 2>();
@@ -124,39 +138,32 @@ screen_product(const double* __restrict__ tab, const double* __restrict__ inj,
         const int nx = kt + STAGES - 1;
         if (nx < nk) load(nx % STAGES, nx);
         else cp_async_commit();
-        const double* ps = Ps + (kt % STAGES) * ROWS * PP;
-        const double* is = Is + (kt % STAGES) * KB * TP + w * TPW;
+        const double* ps = Ps + (kt % STAGES) * ROWS * MPP + (wm * 32 + g) * MPP + tq;
+        const double* is = Is + (kt % STAGES) * KB * TP + tq * TP + wn * NTW * 8 + g;
 #pragma unroll
-        for (int kk = 0; kk < KB; kk += 2) {
-            double2 p[RT];
+        for (int kk = 0; kk < KB; kk += 4) {
+            double a[4], b[NTW];
 #pragma unroll
-            for (int i = 0; i < RT; ++i)
-                p[i] = *reinterpret_cast<const double2*>(ps + (lane + 32 * i) * PP + kk);
+            for (int i = 0; i < 4; ++i) a[i] = ps[i * 8 * MPP + kk];
 #pragma unroll
-            for (int j = 0; j < TPW; j += 2) {
-                const double2 a = *reinterpret_cast<const double2*>(is + kk * TP + j);
-                const double2 b = *reinterpret_cast<const double2*>(is + (kk + 1) * TP + j);
+            for (int j = 0; j < NTW; ++j) b[j] = is[kk * TP + j * 8];
 #pragma unroll
-                for (int i = 0; i < RT; ++i) {
-                    acc[i][j] = __fma_rn(p[i].x, a.x, acc[i][j]);
-                    acc[i][j + 1] = __fma_rn(p[i].x, a.y, acc[i][j + 1]);
-                    acc[i][j] = __fma_rn(p[i].y, b.x, acc[i][j]);
-                    acc[i][j + 1] = __fma_rn(p[i].y, b.y, acc[i][j + 1]);
-                }
-            }
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NTW; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
     }
     cp_async_wait<0>();
 
     double* out = part + ((size_t)split * NT + tb) * L * TP;
 #pragma unroll
-    for (int i = 0; i < RT; ++i) {
-        const int row = row0 + lane + 32 * i;
+    for (int i = 0; i < 4; ++i) {
+        const int row = row0 + wm * 32 + i * 8 + g;
         if (row < L) {
 #pragma unroll
-            for (int j = 0; j < TPW; j += 2)
-                *reinterpret_cast<double2*>(out + (size_t)row * TP + w * TPW + j) =
-                    make_double2(acc[i][j], acc[i][j + 1]);
+            for (int j = 0; j < NTW; ++j)
+                *reinterpret_cast<double2*>(out + (size_t)row * TP + (wn * NTW + j) * 8 + tq * 2) =
+                    make_double2(acc[i][j][0], acc[i][j][1]);
         }
     }
 }
@@ -192,21 +199,19 @@ __global__ void screen_epilogue(const double* __restrict__ part, const double* _
     }
 }
 
-template <int W>
-void launch_product(dim3 grid, cudaStream_t s, const double* tab, const double* inj, double* part,
-                    int L, int Bp, int NT, int kper) {
-    screen_product<W><<<grid, W * 32, product_smem(W), s>>>(tab, inj, part, L, Bp, NT, kper);
+template <int NTW>
+void launch_mma(dim3 grid, int wn, cudaStream_t s, const double* tab, const double* inj,
+                double* part, int L, int Bp, int NT, int kper) {
+    screen_product_mma<NTW><<<grid, 128 * wn, mma_smem(NTW, wn), s>>>(tab, inj, part, L, Bp, NT,
+                                                                      kper, wn);
 }
-
-using ProductFn = void (*)(dim3, cudaStream_t, const double*, const double*, double*, int, int,
-                           int, int);
-const ProductFn kProducts[MAXW] = {launch_product<1>, launch_product<2>, launch_product<3>,
-                                   launch_product<4>, launch_product<5>, launch_product<6>,
-                                   launch_product<7>, launch_product<8>};
-const void* kProductFns[MAXW] = {(const void*)screen_product<1>, (const void*)screen_product<2>,
-                                 (const void*)screen_product<3>, (const void*)screen_product<4>,
-                                 (const void*)screen_product<5>, (const void*)screen_product<6>,
-                                 (const void*)screen_product<7>, (const void*)screen_product<8>};
+using MmaFn = void (*)(dim3, int, cudaStream_t, const double*, const double*, double*, int, int,
+                       int, int);
+const MmaFn kMma[NTW_MAX] = {launch_mma<1>, launch_mma<2>, launch_mma<3>,
+                             launch_mma<4>, launch_mma<5>, launch_mma<6>};
+const void* kMmaFns[NTW_MAX] = {(const void*)screen_product_mma<1>, (const void*)screen_product_mma<2>,
+                                (const void*)screen_product_mma<3>, (const void*)screen_product_mma<4>,
+                                (const void*)screen_product_mma<5>, (const void*)screen_product_mma<6>};
 
 template <typename T> void dfree(T*& p) {
     if (p) cudaFree(p);
@@ -222,7 +227,8 @@ struct hpr_screen {
     double* tab = nullptr;   // NT x L x Bp
     double* lim = nullptr;   // NT x L
     // per-run state (sized for the largest T seen)
-    int T = 0, W = 0, Tp = 0, S = 1, kper = 0, ctas = 0;
+    int T = 0, Tp = 0, S = 1, kper = 0, ctas = 0;
+    int NTW = 1, WN = 1;      // period tiles of 8 per warp, warp rows per CTA
     double tol = 0.0;
     long long cap = 0, found = 0;
     double* inj = nullptr;   // Bp x Tp, zero padded
@@ -252,8 +258,8 @@ struct hpr_screen {
     // bus splits: row tiles x S x NT should fill whole waves of resident CTAs
     void plan() {
         int per_sm = 0;
-        SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kProductFns[W - 1], W * 32,
-                                                          product_smem(W)));
+        SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kMmaFns[NTW - 1], 128 * WN,
+                                                          mma_smem(NTW, WN)));
         if (per_sm < 1) fail(HPR_ERR_CUDA, "screen product kernel does not fit on an SM");
         ctas = per_sm;
         const long long resident = (long long)per_sm * sms;
@@ -268,11 +274,10 @@ struct hpr_screen {
             const long long tiles = row_tiles * se;
             const long long waves = (tiles + resident - 1) / resident;
             const double eff = (double)tiles / (double)(waves * resident);
-            if (eff > best_eff + 0.05) {
+            if (eff > best_eff + 0.02) {   // fewer splits unless clearly better
                 best_eff = eff;
                 best = s;
             }
-            if (eff >= 0.9) break;
         }
         const int kp = (stages + best - 1) / best;
         kper = kp * KB;
@@ -281,7 +286,7 @@ struct hpr_screen {
 
     void launch() {
         dim3 grid((L + ROWS - 1) / ROWS, S, NT);
-        kProducts[W - 1](grid, stream, tab, inj, part, L, Bp, NT, kper);
+        kMma[NTW - 1](grid, WN, stream, tab, inj, part, L, Bp, NT, kper);
         SCK(cudaGetLastError());
     }
     void epilogue() {
@@ -325,9 +330,12 @@ extern "C" int hpr_screen_create(int32_t device, int32_t n_lines, int32_t n_buse
         SCK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
         SCK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         for (auto& e : h->ev) SCK(cudaEventCreate(&e));
-        for (int w = 1; w <= MAXW; ++w)
-            SCK(cudaFuncSetAttribute(kProductFns[w - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)product_smem(w)));
+        for (int t = 1; t <= NTW_MAX; ++t) {
+            SCK(cudaFuncSetAttribute(kMmaFns[t - 1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)mma_smem(t, 2)));
+            SCK(cudaFuncSetAttribute(kMmaFns[t - 1],
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
         const size_t per = (size_t)h->L * h->Bp;
         SCK(cudaMalloc(&h->tab, per * h->NT * sizeof(double)));
         SCK(cudaMalloc(&h->lim, (size_t)h->L * h->NT * sizeof(double)));
@@ -355,12 +363,14 @@ extern "C" int hpr_screen_run(hpr_screen* h, const double* injections, int32_t n
     SCREEN_API_BEGIN
     if (!h || !injections || !n_found) fail(HPR_ERR_INVALID, "hpr_screen_run: null argument");
     if (n_periods <= 0) fail(HPR_ERR_EMPTY, "hpr_screen_run: no periods");
-    if (n_periods > MAXW * TPW)
+    if (n_periods > 2 * NTW_MAX * 8)
         fail(HPR_ERR_INVALID, "hpr_screen_run: more than 96 periods per screen");
     SCK(cudaSetDevice(h->dev));
     h->T = n_periods;
-    h->W = (n_periods + TPW - 1) / TPW;
-    h->Tp = h->W * TPW;
+    const int tiles = (n_periods + 7) / 8;
+    h->WN = (tiles + NTW_MAX - 1) / NTW_MAX;
+    h->NTW = (tiles + h->WN - 1) / h->WN;
+    h->Tp = h->WN * h->NTW * 8;
     h->tol = tol;
     h->plan();
     h->grow(h->inj, h->inj_cap, (size_t)h->Bp * h->Tp);

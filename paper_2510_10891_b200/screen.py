@@ -85,6 +85,13 @@ def injections(point, instance) -> np.ndarray:
     return inj
 
 
+def _ranks(ids) -> np.ndarray:
+    """Position of each id in Python string order (the sort key's tie-breaks)."""
+    r = np.empty(len(ids), np.int64)
+    r[sorted(range(len(ids)), key=ids.__getitem__)] = np.arange(len(ids))
+    return r
+
+
 class FlowScreen:
     """PTDF tables of one ``PtdfTable`` resident on one GPU, with the per-key
     line limits (``Line.limit_for``, ``instance.py:88-89``)."""
@@ -100,6 +107,8 @@ class FlowScreen:
         self.limits = np.ascontiguousarray(
             [[ln.limit_for(k) for ln in lines] for k in self.keys], dtype=np.float64)
         self.shape = (n_l, n_b)
+        self.line_rank = _ranks(self.line_ids)
+        self.key_rank = _ranks(self.keys)
         self._last_t = 0
         ptrs = (C.c_void_p * len(tabs))(*[t.ctypes.data for t in tabs])
         h = C.c_void_p()
@@ -184,10 +193,14 @@ def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) ->
     scr = screen_for(ptdf, instance)
     tab, line, per, flow, exc = scr.run(inj, tol)
     keys, lids, lim = scr.keys, scr.line_ids, scr.limits
-    out = [_VIOLATION_CLASS(line=lids[l], period=int(t), contingency=keys[k], flow=float(f),
-                            limit=float(lim[k, l]), excess=float(e),
-                            already_monitored=(lids[l], int(t), keys[k]) in monitored)
-           for k, l, t, f, e in zip(tab.tolist(), line.tolist(), per.tolist(), flow.tolist(),
-                                    exc.tolist())]
-    out.sort(key=lambda v: (-v.excess, v.line, v.period, v.contingency))
+    # the reference's order (driver.py:199): excess descending, then line id,
+    # period and contingency id as strings -- one lexsort over id ranks
+    order = np.lexsort((scr.key_rank[tab], per, scr.line_rank[line], -exc))
+    cls = _VIOLATION_CLASS
+    out = []
+    for k, l, t, f, e in zip(tab[order].tolist(), line[order].tolist(), per[order].tolist(),
+                             flow[order].tolist(), exc[order].tolist()):
+        key, lid = keys[k], lids[l]
+        out.append(cls(lid, t, key, f, float(lim[k, l]), e,
+                       (lid, t, key) in monitored if monitored else False))
     return out
