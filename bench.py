@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--e2e-max-iter", type=int, default=200_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-screen", action="store_true")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"],
                     help="N>1: independent replicas (weak scaling) or one LP row-partitioned "
@@ -174,7 +175,7 @@ def build_lp(args, device):
     from paper_2510_10891_b200 import scuc
     t = time.perf_counter()
     doc, mon, lpa = scuc.build_config(args.config, n_triples=args.triples, device=device)
-    return lpa, time.perf_counter() - t
+    return lpa, time.perf_counter() - t, doc
 
 
 def bytes_model(m, n, nnz, s):
@@ -216,6 +217,62 @@ def cpu_baseline_sample(lpa, lam, sigma, precision):
     return BLOCK / el, el
 
 
+FP64_TFLOPS_NOMINAL = 37.0   # B200 datasheet FP64 / FP64 tensor; MEASURED_PEAKS has no FP64 figure
+
+
+def screen_leg(doc, x, reps):
+    """The post-MILP flow screen (driver.screen_violations, driver.py:165-200;
+    SURVEY 8(f) rank 3) on the config's base-case PTDF at the e2e LP point:
+    device product/epilogue times (CUDA events, inputs resident), the public
+    call end to end (host point in, sorted Violation list out), and the host
+    BLAS product the reference runs (driver.py:186) timed beside it."""
+    import numpy as np
+    from paper_2510_10891_b200 import scuc, screen
+    t0 = time.perf_counter()
+    net = scuc.Instance(doc).net
+    tab = scuc._ptdf_rows_direct(net.n_b, net.fb, net.tb, net.react, net.ref,
+                                 list(range(len(net.fb))), device="cuda")
+    t_ptdf = time.perf_counter() - t0
+    inst = screen.instance_view(doc)
+    ptdf = screen.Tables({"base": tab})
+    t0 = time.perf_counter()
+    first = screen.screen_violations(x, inst, ptdf)          # uploads the table once
+    t_first = time.perf_counter() - t0
+    walls = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        v = screen.screen_violations(x, inst, ptdf)
+        walls.append(time.perf_counter() - t0)
+    scr = screen.screen_for(ptdf, inst)
+    us_p, us_e = scr.bench(reps)
+    info = scr.info()
+    n_l, n_b = tab.shape
+    n_t = doc["time_periods"]
+    tp = -(-n_t // 8) * 8
+    nbytes = n_l * n_b * 8 + n_b * tp * 8 + info["splits"] * n_l * tp * 8
+    flops = 2.0 * n_l * n_b * n_t
+    inj = screen.injections(x, inst)
+    t0 = time.perf_counter()
+    _ = tab @ inj
+    cpu_s = time.perf_counter() - t0
+    scr.close()
+    tfl = flops / us_p / 1e6
+    return {"workload": f"base-case screen: {n_l} lines x {n_b} buses x {n_t} periods "
+                        f"(FP64 PTDF {n_l * n_b * 8 / 1e9:.2f} GB resident), e2e LP point",
+            "violations": len(v), "same_as_first": [w.triple for w in v] == [w.triple for w in first],
+            "product_us": us_p, "epilogue_us": us_e, "splits": info["splits"],
+            "roofline": {"bound": "fp64", "achieved": tfl, "peak": FP64_TFLOPS_NOMINAL,
+                         "unit": "TFLOP/s", "frac": tfl / FP64_TFLOPS_NOMINAL,
+                         "peak_kind": "datasheet", "hbm_gbs": nbytes / us_p / 1e3,
+                         "hbm_frac": nbytes / us_p / 1e3 / measured_peak_hbm()[0],
+                         "bytes_per_launch": nbytes, "flops_per_launch": flops},
+            "e2e_s": float(np.median(walls)), "first_call_s": t_first, "ptdf_build_s": t_ptdf,
+            "cpu_baseline": {"value": cpu_s, "unit": "s", "cores": os.cpu_count(),
+                             "kind": "reference",
+                             "sample": "numpy table @ injections (driver.py:186), host BLAS, "
+                                       "product only (the reference's per-entry loop not timed)"}}
+
+
 def run_b200(args):
     import torch
     ws, rank, local = dist_env()
@@ -226,7 +283,7 @@ def run_b200(args):
     from paper_2510_10891_b200 import hprlp
     from paper_2510_10891_b200.lp import Precision
 
-    lpa, t_build = build_lp(args, f"cuda:{local}")
+    lpa, t_build, doc = build_lp(args, f"cuda:{local}")
     m, n = lpa.shape
     nnz = lpa.nnz
     s = 8 if args.precision == "fp64" else 4
@@ -399,6 +456,12 @@ def run_b200(args):
                                "status": r32.status.value, "objective": r32.objective,
                                "rel_kkt": r32.kkt.max_rel,
                                "fp64_fallback": bool(getattr(r32, "fp64_fallback", False))}
+    if rank == 0 and not args.no_screen:
+        try:
+            xs = res.x if not args.no_e2e else np.zeros(n)
+            out["screen"] = screen_leg(doc, xs, args.kernel_reps)
+        except Exception as exc:          # recorded, never silently replaced
+            out["screen"] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0 and not args.no_cpu_baseline:
         v, el = cpu_baseline_sample(lpa, st0.lam, st.sigma_final, args.precision)
         out["cpu_baseline"] = {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",

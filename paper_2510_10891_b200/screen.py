@@ -24,6 +24,7 @@ screen raises.
 from __future__ import annotations
 
 import ctypes as C
+import types
 import weakref
 from dataclasses import dataclass
 
@@ -152,6 +153,49 @@ class FlowScreen:
         a, b = C.c_double(), C.c_double()
         _capi.check(self.lib.hpr_screen_bench(self.handle, reps, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+
+class _Line:
+    __slots__ = ("lid", "limit", "emergency_limit")
+
+    def __init__(self, d):
+        self.lid, self.limit, self.emergency_limit = d["id"], d["limit"], d["emergency_limit"]
+
+    def limit_for(self, key):                      # instance.py:88-89
+        return self.limit if key == "base" else self.emergency_limit
+
+
+def instance_view(doc: dict):
+    """The attributes ``screen_violations`` reads from a ``ScucInstance``
+    (``instance.py:99-139``), taken from a reference-schema instance document
+    (for callers that hold the document but not a parsed instance)."""
+    gens = tuple(types.SimpleNamespace(gid=g["id"], bus=g["bus"], p_min=g["p_min"],
+                                       p_max=g["p_max"], n_segments=len(g["segments"]))
+                 for g in doc["generators"])
+    buses = tuple(types.SimpleNamespace(bid=b["id"], demand=b["demand"]) for b in doc["buses"])
+    lines = tuple(_Line(ln) for ln in doc["lines"])
+    conts = tuple(types.SimpleNamespace(cid=c["id"]) for c in doc.get("contingencies", ()))
+    net = types.SimpleNamespace(buses=buses, lines=lines, contingencies=conts,
+                                bus_index=lambda: {b.bid: i for i, b in enumerate(buses)})
+    return types.SimpleNamespace(
+        generators=gens, buses=buses, lines=lines, contingencies=conts, network=net,
+        n_periods=doc["time_periods"],
+        demand_matrix=lambda: np.array([b.demand for b in buses], dtype=np.float64),
+        contingency_keys=lambda: ["base"] + [c.cid for c in conts])
+
+
+class Tables:
+    """``PtdfTable``'s read interface (``instance.py:166-168``) over a dict of
+    (n_lines x n_buses) arrays keyed by contingency key."""
+
+    def __init__(self, tables: dict):
+        self._t = dict(tables)
+
+    def keys(self) -> list:
+        return list(self._t)
+
+    def table(self, key: str = "base"):
+        return self._t[key]
 
 
 _SCREENS: dict = {}

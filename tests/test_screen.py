@@ -11,7 +11,6 @@ through the same Python signature, plus the contract's error behaviour."""
 
 import json
 import os
-import types
 
 import numpy as np
 import pytest
@@ -28,39 +27,12 @@ def golden():
     return np.load(GOLD)
 
 
-class _Line:
-    def __init__(self, d):
-        self.lid, self.limit, self.emergency_limit = d["id"], d["limit"], d["emergency_limit"]
-
-    def limit_for(self, key):                      # instance.py:88-89
-        return self.limit if key == "base" else self.emergency_limit
+_Line = screen._Line
+instance_of = screen.instance_view
 
 
-def instance_of(doc):
-    """The attributes screen_violations reads from a ScucInstance
-    (instance.py:99-139), built from the golden document."""
-    gens = tuple(types.SimpleNamespace(gid=g["id"], bus=g["bus"], p_min=g["p_min"],
-                                       n_segments=len(g["segments"])) for g in doc["generators"])
-    buses = tuple(types.SimpleNamespace(bid=b["id"], demand=b["demand"]) for b in doc["buses"])
-    lines = tuple(_Line(ln) for ln in doc["lines"])
-    conts = tuple(types.SimpleNamespace(cid=c["id"]) for c in doc["contingencies"])
-    net = types.SimpleNamespace(buses=buses, lines=lines, contingencies=conts,
-                                bus_index=lambda: {b.bid: i for i, b in enumerate(buses)})
-    return types.SimpleNamespace(
-        generators=gens, buses=buses, lines=lines, contingencies=conts, network=net,
-        n_periods=doc["time_periods"],
-        demand_matrix=lambda: np.array([b.demand for b in buses], dtype=np.float64),
-        contingency_keys=lambda: ["base"] + [c.cid for c in conts])
-
-
-class _Ptdf:
-    """PtdfTable's read interface (instance.py:141-173) over the golden tables."""
-
-    def __init__(self, keys, tables):
-        self._t = dict(zip(keys, tables))
-
-    def table(self, key="base"):
-        return self._t[key]
+def _Ptdf(keys, tables):
+    return screen.Tables(dict(zip(keys, tables)))
 
 
 def case(g, ci):
@@ -189,3 +161,51 @@ def test_device_screen_sizes_and_edges():
         tb, *_ = scr.run(inj * 0.0, 1e-4)
         assert len(tb) == 0
         scr.close()
+
+
+def _scuckit():
+    import sys
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "scuckit")) and p not in sys.path:
+            sys.path.append(p)
+    try:
+        import scuckit  # noqa: F401
+        return True
+    except Exception:
+        return False
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not _scuckit(), reason="reference package not installed")
+def test_install_routes_driver_screen():
+    """After hprlp.install() the driver's name lookup (driver.py:288) reaches
+    the device screen, which takes the reference's own ScucInstance and
+    PtdfTable (read-only arrays) and returns its Violation class."""
+    import scuckit
+    import scuckit.driver as drv
+    from scuckit import compute_ptdf, parse_instance
+    from paper_2510_10891_b200 import hprlp, scuc
+    ref_fn = drv.screen_violations
+    doc = scuc.generate_instance(30, 10, 41, 24, seed=9, n_contingencies=6)
+    inst = parse_instance(doc)
+    ptdf = compute_ptdf(inst.network)
+    u, pp, pen, n_cols = screen.column_blocks(inst)
+    rng = np.random.default_rng(2)
+    x = np.zeros(n_cols)
+    x[u] = 1.0
+    x[pp] = rng.uniform(0, 1, size=u.shape) * np.array(
+        [[g.p_max - g.p_min] for g in inst.generators])
+    want = ref_fn(x, inst, ptdf, tol=1e-4)
+    hprlp.install()
+    try:
+        assert drv.screen_violations is screen.screen_violations
+        assert scuckit.screen_violations is screen.screen_violations
+        got = drv.screen_violations(x, inst, ptdf, tol=1e-4)
+        assert all(type(v) is drv.Violation for v in got)
+    finally:
+        hprlp.uninstall()
+    assert drv.screen_violations is ref_fn
+    ref = [[v.line, v.period, v.contingency, v.flow, v.limit, v.excess, v.already_monitored]
+           for v in want]
+    tabs = np.stack([ptdf.table(k) for k in inst.contingency_keys()])
+    _compare(got, ref, tabs, screen.injections(x, inst))

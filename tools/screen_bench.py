@@ -24,7 +24,6 @@ sys.path.insert(0, ROOT)
 
 from oracle import screen_oracle  # noqa: E402  (CPU baseline leg only)
 from paper_2510_10891_b200 import scuc, screen  # noqa: E402
-from tests.test_screen import _Ptdf, instance_of  # noqa: E402
 
 HBM_GBS = 6548.2
 FP64_TFLOPS_NOMINAL = 37.0   # B200 datasheet FP64 (= FP64 tensor); no measured figure in MEASURED_PEAKS
@@ -52,8 +51,8 @@ def main():
     doc = scuc.generate_instance(a.buses, a.gens, a.lines, a.periods, seed=a.seed)
     tab = full_ptdf(doc, "cuda")
     t_build = time.perf_counter() - t0
-    inst = instance_of(doc)
-    ptdf = _Ptdf(["base"], [tab])
+    inst = screen.instance_view(doc)
+    ptdf = screen.Tables({"base": tab})
 
     # a dispatch that loads the network: every unit on at 80-100% of p_max
     from paper_2510_10891_b200 import screen as S
@@ -76,7 +75,7 @@ def main():
     us_prod, us_epi = scr.bench(a.reps)
     info = scr.info()
     L, B, T = a.lines, a.buses, a.periods
-    tp = -(-T // 12) * 12
+    tp = -(-T // 8) * 8
     bytes_prod = L * B * 8 + B * T * 8 + info["splits"] * L * tp * 8
     flops = 2.0 * L * B * T
     gbs = bytes_prod / us_prod / 1e3
@@ -102,7 +101,7 @@ def main():
                                    [ln.lid for ln in inst.lines], inj, (), 1e-4)
         out["cpu_screen_s"] = time.perf_counter() - t1
         out["cpu_threads"] = os.cpu_count()
-        out["cpu_same_triples"] = [r[:3] for r in ref] == [w.triple for w in v]
+        out["cpu_same_triple_set"] = {r[:3] for r in ref} == {w.triple for w in v}
         out["max_flow_diff"] = float(np.abs(scr.flows(0) - flows).max())
     print(json.dumps(out))
 
