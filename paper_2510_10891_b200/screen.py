@@ -51,6 +51,7 @@ class Violation:
 
 
 _VIOLATION_CLASS = Violation
+PERIODS_PER_LAUNCH = 96   # hpr_screen_run's limit (2 warp rows x 6 period tiles of 8)
 
 
 def column_blocks(instance):
@@ -128,23 +129,35 @@ class FlowScreen:
 
     def run(self, inj: np.ndarray, tol: float):
         """Screen an (n_buses x n_periods) injection matrix; returns the
-        records (table, line, period, flow, excess) as numpy arrays."""
+        records (table, line, period, flow, excess) as numpy arrays.  The
+        kernel takes up to PERIODS_PER_LAUNCH periods; longer horizons run
+        in period chunks (each (line, period) entry is independent)."""
         inj = np.ascontiguousarray(inj, dtype=np.float64)
         if inj.ndim != 2 or inj.shape[0] != self.shape[1]:
             raise ValueError("injections must be (n_buses, n_periods)")
-        n = C.c_int64()
-        _capi.check(self.lib.hpr_screen_run(self.handle, _capi.ptr(inj), inj.shape[1],
-                                            float(tol), C.byref(n)))
-        self._last_t = inj.shape[1]
-        k = n.value
-        rec = (np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k, np.int32),
-               np.empty(k, np.float64), np.empty(k, np.float64))
-        _capi.check(self.lib.hpr_screen_fetch(self.handle, *[_capi.ptr(a) for a in rec]))
-        return rec
+        n_t = inj.shape[1]
+        parts = []
+        for t0 in range(0, max(n_t, 1), PERIODS_PER_LAUNCH):
+            chunk = np.ascontiguousarray(inj[:, t0:t0 + PERIODS_PER_LAUNCH])
+            n = C.c_int64()
+            _capi.check(self.lib.hpr_screen_run(self.handle, _capi.ptr(chunk), chunk.shape[1],
+                                                float(tol), C.byref(n)))
+            k = n.value
+            rec = (np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k, np.int32),
+                   np.empty(k, np.float64), np.empty(k, np.float64))
+            _capi.check(self.lib.hpr_screen_fetch(self.handle, *[_capi.ptr(a) for a in rec]))
+            rec[2][:] += t0
+            parts.append(rec)
+        self._last_t = n_t if n_t <= PERIODS_PER_LAUNCH else -1
+        if len(parts) == 1:
+            return parts[0]
+        return tuple(np.concatenate([p[i] for p in parts]) for i in range(5))
 
     def flows(self, table: int = 0) -> np.ndarray:
         """Flows of one table from the last run (``PtdfTable.flows``,
         ``instance.py:170-173``)."""
+        if self._last_t < 0:
+            raise ValueError("flows() holds only the last period chunk of a long horizon")
         out = np.empty((self.shape[0], self._last_t), np.float64)
         _capi.check(self.lib.hpr_screen_flows(self.handle, table, _capi.ptr(out)))
         return out

@@ -161,6 +161,19 @@ def test_device_screen_sizes_and_edges():
         tb, *_ = scr.run(inj * 0.0, 1e-4)
         assert len(tb) == 0
         scr.close()
+    # a horizon longer than one launch (200 periods) runs in period chunks
+    tab = rng.standard_normal((70, 50)) * 0.2
+    inj = rng.standard_normal((50, 200)) * 50
+    lim = np.full(70, 30.0)
+    lines = [_Line({"id": f"l{i}", "limit": 30.0, "emergency_limit": 30.0}) for i in range(70)]
+    scr = screen.FlowScreen(_Ptdf(["base"], [tab]), ["base"], lines)
+    tb, li, pe, fl, ex = scr.run(inj, 0.0)
+    flows = tab @ inj
+    want = set(zip(*np.nonzero(np.abs(flows) - lim[:, None] > 1e-9)))
+    got = set(zip(li.tolist(), pe.tolist()))
+    assert want <= got and pe.max() >= 96
+    np.testing.assert_allclose(fl, flows[li, pe], rtol=0, atol=1e-9)
+    scr.close()
 
 
 def _scuckit():
