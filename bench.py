@@ -254,7 +254,13 @@ def screen_leg(doc, x, reps):
     inj = screen.injections(x, inst)
     t0 = time.perf_counter()
     _ = tab @ inj
+    gemm_s = time.perf_counter() - t0
+    from oracle import screen_oracle       # CPU baseline leg only
+    t0 = time.perf_counter()
+    ref = screen_oracle.screen([tab], [[ln.limit for ln in inst.lines]], ["base"],
+                               [ln.lid for ln in inst.lines], inj, (), 1e-4)
     cpu_s = time.perf_counter() - t0
+    set_diff = len({r[:3] for r in ref} ^ {w.triple for w in v})
     scr.close()
     tfl = flops / us_p / 1e6
     return {"workload": f"base-case screen: {n_l} lines x {n_b} buses x {n_t} periods "
@@ -267,10 +273,12 @@ def screen_leg(doc, x, reps):
                          "hbm_frac": nbytes / us_p / 1e3 / measured_peak_hbm()[0],
                          "bytes_per_launch": nbytes, "flops_per_launch": flops},
             "e2e_s": float(np.median(walls)), "first_call_s": t_first, "ptdf_build_s": t_ptdf,
+            "oracle_set_diff": set_diff,        # triples in one list but not the other
             "cpu_baseline": {"value": cpu_s, "unit": "s", "cores": os.cpu_count(),
-                             "kind": "reference",
-                             "sample": "numpy table @ injections (driver.py:186), host BLAS, "
-                                       "product only (the reference's per-entry loop not timed)"}}
+                             "kind": "port", "gemm_only_s": gemm_s,
+                             "sample": "oracle/screen_oracle.py on the same point: numpy "
+                                       "table @ injections with host BLAS (all cores), then the "
+                                       "reference's per-(line, period) loop and sort (one core)"}}
 
 
 def run_b200(args):
