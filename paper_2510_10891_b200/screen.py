@@ -247,6 +247,8 @@ def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) ->
     same signature, errors and result order as ``driver.py:165-200``."""
     inj = injections(point, instance)
     monitored = set(monitored)
+    if len(instance.lines) == 0 or inj.shape[1] == 0:
+        return []                     # nothing to screen (the reference's loops are empty)
     scr = screen_for(ptdf, instance)
     tab, line, per, flow, exc = scr.run(inj, tol)
     keys, lids, lim = scr.keys, scr.line_ids, scr.limits

@@ -86,3 +86,18 @@ def test_c_caller_links_and_presolves(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip().endswith("ok")
+
+
+def test_screen_abi_errors_without_gpu():
+    """include/hpr_screen.h: argument errors are codes with a message, checked
+    before any device call (so they hold on a CPU-only host too)."""
+    lib = _capi.load()
+    h = ctypes.c_void_p()
+    assert lib.hpr_screen_create(0, 4, 4, 1, None, None, ctypes.byref(h)) == _capi.HPR_ERR_INVALID
+    assert b"null" in lib.hpr_last_error()
+    n = ctypes.c_int64()
+    assert lib.hpr_screen_run(None, None, 24, 1e-4, ctypes.byref(n)) == _capi.HPR_ERR_INVALID
+    assert lib.hpr_screen_fetch(None, None, None, None, None, None) == _capi.HPR_ERR_INVALID
+    assert lib.hpr_screen_flows(None, 0, None) == _capi.HPR_ERR_INVALID
+    assert ctypes.sizeof(_capi.ScreenInfo) == 6 * 4 + 8
+    lib.hpr_screen_destroy(None)            # no-op
