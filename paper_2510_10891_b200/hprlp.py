@@ -505,6 +505,30 @@ def solve(lp, config=None, start=None):
     return result
 
 
+def solve_many(lps, config=None, starts=None, workers: int | None = None) -> list:
+    """Several independent LP solves on one GPU at once (SURVEY §8(f) rank 4:
+    the node LPs of a branch-and-bound frontier, ``milp_bb.py:204-253``, or
+    any set of fixing-round LPs).  Each LP gets its own engine, so its own
+    CUDA stream and graph (``hprlp_b200.h``: distinct handles are
+    independent); one host thread per solve drives it, and ctypes releases
+    the GIL inside the C-ABI, so the solves overlap on the device.  Each
+    result is exactly what :func:`solve` returns for that LP alone (same
+    kernels, same per-LP order of operations); only the wall clock is shared.
+    Small LPs (C1/C2 size) run in the engine's launch-latency regime, which
+    is where overlapping several of them pays."""
+    from concurrent.futures import ThreadPoolExecutor
+    lps = list(lps)
+    if starts is None:
+        starts = [None] * len(lps)
+    if len(starts) != len(lps):
+        raise ValueError("starts must match lps")
+    if not lps:
+        return []
+    workers = max(1, min(workers or 8, len(lps)))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(lambda a: solve(a[0], config, a[1]), zip(lps, starts)))
+
+
 def write_iteration_log(path, result, solve_id: str = "solve") -> None:
     """``hprlp.write_iteration_log`` (hprlp.py:303-316)."""
     import csv
