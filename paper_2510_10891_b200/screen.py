@@ -256,10 +256,12 @@ def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) ->
     # period and contingency id as strings -- one lexsort over id ranks
     order = np.lexsort((scr.key_rank[tab], per, scr.line_rank[line], -exc))
     cls = _VIOLATION_CLASS
-    out = []
-    for k, l, t, f, e in zip(tab[order].tolist(), line[order].tolist(), per[order].tolist(),
-                             flow[order].tolist(), exc[order].tolist()):
-        key, lid = keys[k], lids[l]
-        out.append(cls(lid, t, key, f, float(lim[k, l]), e,
-                       (lid, t, key) in monitored if monitored else False))
+    tab, line, per = tab[order], line[order], per[order]
+    cols = (tab.tolist(), line.tolist(), per.tolist(), flow[order].tolist(),
+            lim[tab, line].tolist(), exc[order].tolist())
+    if monitored:
+        out = [cls(lids[l], t, keys[k], f, li, e, (lids[l], t, keys[k]) in monitored)
+               for k, l, t, f, li, e in zip(*cols)]
+    else:
+        out = [cls(lids[l], t, keys[k], f, li, e, False) for k, l, t, f, li, e in zip(*cols)]
     return out
