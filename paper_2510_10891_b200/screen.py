@@ -214,11 +214,12 @@ class Tables:
 _SCREENS: dict = {}
 
 
-def screen_for(ptdf, instance, device: int = 0) -> FlowScreen:
+def screen_for(ptdf, instance, device: int = 0, keys=None) -> FlowScreen:
     """The resident screen of ``ptdf`` (built once; ``PtdfTable`` is
     immutable, ``instance.py:141-147``), rebuilt only if the instance's keys
-    or limits differ from the ones it was built with."""
-    keys = instance.contingency_keys()
+    or limits differ from the ones it was built with.  ``keys`` restricts the
+    resident tables to a subset of the instance's keys (one rank's shard)."""
+    keys = list(instance.contingency_keys() if keys is None else keys)
     ent = _SCREENS.get(id(ptdf))
     if ent is not None:
         ref, scr = ent
@@ -242,6 +243,22 @@ def _drop(key):
         ent[1].close()
 
 
+def _assemble(recs, keys, lids, lim, line_rank, key_rank, monitored) -> list:
+    """Violation objects in the reference's order (driver.py:199): excess
+    descending, then line id, period and contingency id as strings -- one
+    lexsort over id ranks.  ``recs`` = (key index, line, period, flow, excess)."""
+    tab, line, per, flow, exc = recs
+    order = np.lexsort((key_rank[tab], per, line_rank[line], -exc))
+    cls = _VIOLATION_CLASS
+    tab, line, per = tab[order], line[order], per[order]
+    cols = (tab.tolist(), line.tolist(), per.tolist(), flow[order].tolist(),
+            lim[tab, line].tolist(), exc[order].tolist())
+    if monitored:
+        return [cls(lids[l], t, keys[k], f, li, e, (lids[l], t, keys[k]) in monitored)
+                for k, l, t, f, li, e in zip(*cols)]
+    return [cls(lids[l], t, keys[k], f, li, e, False) for k, l, t, f, li, e in zip(*cols)]
+
+
 def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) -> list:
     """Flow check of a primal vector over every (line, period, contingency);
     same signature, errors and result order as ``driver.py:165-200``."""
@@ -250,18 +267,49 @@ def screen_violations(point, instance, ptdf, monitored=(), tol: float = 1e-4) ->
     if len(instance.lines) == 0 or inj.shape[1] == 0:
         return []                     # nothing to screen (the reference's loops are empty)
     scr = screen_for(ptdf, instance)
-    tab, line, per, flow, exc = scr.run(inj, tol)
-    keys, lids, lim = scr.keys, scr.line_ids, scr.limits
-    # the reference's order (driver.py:199): excess descending, then line id,
-    # period and contingency id as strings -- one lexsort over id ranks
-    order = np.lexsort((scr.key_rank[tab], per, scr.line_rank[line], -exc))
-    cls = _VIOLATION_CLASS
-    tab, line, per = tab[order], line[order], per[order]
-    cols = (tab.tolist(), line.tolist(), per.tolist(), flow[order].tolist(),
-            lim[tab, line].tolist(), exc[order].tolist())
-    if monitored:
-        out = [cls(lids[l], t, keys[k], f, li, e, (lids[l], t, keys[k]) in monitored)
-               for k, l, t, f, li, e in zip(*cols)]
+    recs = scr.run(inj, tol)
+    return _assemble(recs, scr.keys, scr.line_ids, scr.limits, scr.line_rank, scr.key_rank,
+                     monitored)
+
+
+def shard_keys(keys, world_size: int, rank: int) -> list:
+    """The contingency keys one rank screens: round robin over the
+    instance's key order (each key's product is independent, driver.py:184-186)."""
+    return [k for i, k in enumerate(keys) if i % world_size == rank]
+
+
+def screen_violations_sharded(point, instance, ptdf, monitored=(), tol: float = 1e-4,
+                              group=None, device: int | None = None, _run=None) -> list:
+    """``screen_violations`` with the contingency keys sharded over the ranks
+    of a ``torch.distributed`` group, one GPU per rank (SURVEY §8(e) for the
+    screen: independent products, so no data-path collective).  Each rank
+    keeps only its shard's tables resident and screens them; the violation
+    records are all-gathered once and every rank returns the same list, in
+    the reference's order.  ``_run(keys, inj, tol)`` replaces the device
+    screen of a shard (tests only)."""
+    import torch.distributed as dist
+    ws, rank = dist.get_world_size(group), dist.get_rank(group)
+    inj = injections(point, instance)
+    monitored = set(monitored)
+    keys = list(instance.contingency_keys())
+    if len(instance.lines) == 0 or inj.shape[1] == 0:
+        return []
+    mine = shard_keys(keys, ws, rank)
+    if not mine:
+        local = tuple(np.empty(0, t) for t in (np.int32, np.int32, np.int32, np.float64,
+                                               np.float64))
+    elif _run is not None:
+        local = _run(mine, inj, tol)
     else:
-        out = [cls(lids[l], t, keys[k], f, li, e, False) for k, l, t, f, li, e in zip(*cols)]
-    return out
+        if device is None:
+            import torch
+            device = torch.cuda.current_device()
+        local = screen_for(ptdf, instance, device=device, keys=mine).run(inj, tol)
+    pos = np.array([keys.index(k) for k in mine] or [0], dtype=np.int32)
+    local = (pos[local[0]],) + tuple(local[1:])
+    parts = [None] * ws
+    dist.all_gather_object(parts, local, group=group)
+    recs = tuple(np.concatenate([p[i] for p in parts]) for i in range(5))
+    lids = [ln.lid for ln in instance.lines]
+    lim = np.array([[ln.limit_for(k) for ln in instance.lines] for k in keys], dtype=np.float64)
+    return _assemble(recs, keys, lids, lim, _ranks(lids), _ranks(keys), monitored)

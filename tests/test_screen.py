@@ -222,3 +222,88 @@ def test_install_routes_driver_screen():
            for v in want]
     tabs = np.stack([ptdf.table(k) for k in inst.contingency_keys()])
     _compare(got, ref, tabs, screen.injections(x, inst))
+
+
+def _oracle_run(ci):
+    """A shard's records from numpy products (stands in for the device screen
+    in the CPU gloo test; the merge and ordering are what is under test)."""
+    g = golden()
+    _, inst, _, _ = case(g, ci)
+    keys = inst.contingency_keys()
+    tabs, lims = g[f"c{ci}_tables"], g[f"c{ci}_limits"]
+
+    def run(mine, inj, tol):
+        out = [[], [], [], [], []]
+        for j, key in enumerate(mine):
+            k = keys.index(key)
+            flows = tabs[k] @ inj
+            ex = np.abs(flows) - lims[k][:, None]
+            li, pe = np.nonzero(ex > tol * lims[k][:, None])
+            for a, v in zip(out, (np.full(li.size, j), li, pe, flows[li, pe], ex[li, pe])):
+                a.append(v)
+        return tuple(np.concatenate(a).astype(t) for a, t in
+                     zip(out, (np.int32, np.int32, np.int32, np.float64, np.float64)))
+    return run
+
+
+def _shard_worker(rank, ws, port, ci, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        g = golden()
+        _, inst, ptdf, tol = case(g, ci)
+        res = []
+        for x, mon, _ in points(g, ci):
+            got = screen.screen_violations_sharded(x, inst, ptdf, monitored=mon, tol=tol,
+                                                   _run=_oracle_run(ci))
+            res.append([[v.line, v.period, v.contingency, v.flow, v.limit, v.excess,
+                         v.already_monitored] for v in got])
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_sharded_screen_gloo_matches_reference(ws):
+    """Keys sharded round robin over ws gloo ranks; every rank returns the
+    reference's exact list (golden case 3: 13 keys)."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, ws, port, 3, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    refs = [r for _, _, r in points(golden(), 3)]
+    for _, res in out:
+        assert res == refs
+    assert screen.shard_keys(list("abcde"), 2, 1) == ["b", "d"]
+
+
+@pytest.mark.gpu
+def test_sharded_screen_single_rank_device():
+    """The sharded entry with its device screen (one rank, gloo group)."""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        g = golden()
+        doc, inst, ptdf, tol = case(g, 1)
+        for x, mon, ref in points(g, 1):
+            got = screen.screen_violations_sharded(x, inst, ptdf, monitored=mon, tol=tol, device=0)
+            _compare(got, ref, g["c1_tables"], screen.injections(x, inst))
+    finally:
+        dist.destroy_process_group()
