@@ -41,8 +41,14 @@ void hpr_internal_set_error(const char* msg);  // hpr_engine.cu (hpr_last_error)
 namespace {
 
 constexpr int ROWS = 128;         // lines per CTA (4 warps x 32)
-constexpr int KB = 16;            // buses per pipeline stage
-constexpr int STAGES = 3;
+#ifndef SCREEN_KB
+#define SCREEN_KB 16
+#endif
+#ifndef SCREEN_STAGES
+#define SCREEN_STAGES 3
+#endif
+constexpr int KB = SCREEN_KB;          // buses per pipeline stage
+constexpr int STAGES = SCREEN_STAGES;
 
 struct ScreenErr {
     int code;
