@@ -67,6 +67,10 @@ int hpr_screen_bench(hpr_screen* h, int32_t reps, double* us_product, double* us
 
 int hpr_screen_info_get(hpr_screen* h, hpr_screen_info* info);
 
+/* Measured FP64 tensor-pipe ceiling of the device (register-only DMMA chains,
+ * CUDA events): the roofline peak the screen product is reported against. */
+int hpr_fp64_peak_bench(int32_t device, double* tflops);
+
 void hpr_screen_destroy(hpr_screen* h);
 
 #ifdef __cplusplus

@@ -33,7 +33,8 @@ EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_crea
            "hpr_presolve_run", "hpr_presolve_info", "hpr_presolve_fetch", "hpr_presolve_free",
            # include/hpr_screen.h (device flow screen)
            "hpr_screen_create", "hpr_screen_run", "hpr_screen_fetch", "hpr_screen_flows",
-           "hpr_screen_bench", "hpr_screen_info_get", "hpr_screen_destroy")
+           "hpr_screen_bench", "hpr_screen_info_get", "hpr_screen_destroy",
+           "hpr_fp64_peak_bench")
 
 _p = C.c_void_p
 
@@ -162,6 +163,7 @@ def load(path: str | None = None):
     lib.hpr_screen_info_get.argtypes = [_p, C.POINTER(ScreenInfo)]
     lib.hpr_screen_destroy.argtypes = [_p]
     lib.hpr_screen_destroy.restype = None
+    lib.hpr_fp64_peak_bench.argtypes = [C.c_int32, C.POINTER(C.c_double)]
     _LIB = lib
     return lib
 

@@ -205,6 +205,23 @@ __global__ void screen_epilogue(const double* __restrict__ part, const double* _
     }
 }
 
+// FP64 tensor-pipe ceiling: every warp runs independent DMMA chains on
+// registers only (no memory traffic), so the rate is the pipe's own.
+constexpr int PEAK_CHAINS = 8;
+__global__ void __launch_bounds__(256) dmma_peak(double* sink, int iters) {
+    double c[PEAK_CHAINS][2];
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * blockIdx.x;
+#pragma unroll
+    for (int i = 0; i < PEAK_CHAINS; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < PEAK_CHAINS; ++i) dmma(c[i][0], c[i][1], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < PEAK_CHAINS; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) sink[0] = s;   // keeps the chains live
+}
+
 template <int NTW>
 void launch_mma(dim3 grid, int wn, cudaStream_t s, const double* tab, const double* inj,
                 double* part, int L, int Bp, int NT, int kper) {
@@ -468,6 +485,34 @@ extern "C" int hpr_screen_info_get(hpr_screen* h, hpr_screen_info* info) {
     info->splits = h->S;
     info->ctas_per_sm = h->ctas;
     info->table_bytes = (size_t)h->NT * h->L * h->Bp * sizeof(double);
+    SCREEN_API_END
+}
+
+extern "C" int hpr_fp64_peak_bench(int32_t device, double* tflops) {
+    SCREEN_API_BEGIN
+    if (!tflops) fail(HPR_ERR_INVALID, "hpr_fp64_peak_bench: null argument");
+    SCK(cudaSetDevice(device));
+    int sms = 0;
+    SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* sink = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    SCK(cudaMalloc(&sink, sizeof(double)));
+    SCK(cudaEventCreate(&e0));
+    SCK(cudaEventCreate(&e1));
+    const int blocks = sms * 4, threads = 256, iters = 4096;
+    dmma_peak<<<blocks, threads>>>(sink, 64);   // warm
+    SCK(cudaGetLastError());
+    SCK(cudaEventRecord(e0));
+    dmma_peak<<<blocks, threads>>>(sink, iters);
+    SCK(cudaEventRecord(e1));
+    SCK(cudaEventSynchronize(e1));
+    float ms = 0;
+    SCK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    const double mmas = (double)blocks * (threads / 32) * iters * PEAK_CHAINS;
+    *tflops = mmas * 2.0 * 8 * 8 * 4 / (ms * 1e-3) / 1e12;
     SCREEN_API_END
 }
 

@@ -211,6 +211,13 @@ class Tables:
         return self._t[key]
 
 
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured FP64 tensor-pipe ceiling (``hpr_fp64_peak_bench``)."""
+    v = C.c_double()
+    _capi.check(_capi.load().hpr_fp64_peak_bench(device, C.byref(v)))
+    return v.value
+
+
 _SCREENS: dict = {}
 
 

@@ -307,3 +307,10 @@ def test_sharded_screen_single_rank_device():
             _compare(got, ref, g["c1_tables"], screen.injections(x, inst))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fp64_peak_probe_is_plausible():
+    """The measured DMMA ceiling the bench's screen roofline divides by."""
+    v = screen.fp64_peak_tflops()
+    assert 5.0 < v < 100.0
