@@ -82,6 +82,11 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // B (4 buses x 8 periods) from the injection tile, both at the minimum two
 // wavefronts per load.
 constexpr int MPP = KB + 4;
+#ifndef SCREEN_WARP_MT
+#define SCREEN_WARP_MT 4     // 8-line m-tiles per warp
+#endif
+constexpr int WMT = SCREEN_WARP_MT;
+constexpr int WM = ROWS / (8 * WMT);   // warps along the lines of a CTA
 constexpr int NTW_MAX = 6;
 size_t mma_smem(int ntw, int wn) {
     return (size_t)STAGES * (ROWS * MPP + KB * wn * ntw * 8) * sizeof(double);
@@ -109,7 +114,7 @@ screen_product_mma(const double* __restrict__ tab, const double* __restrict__ in
     const int k0 = split * kper;
     const int nk = min(kper, Bp - k0) / KB;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, tq = lane & 3;
+    const int wm = warp % WM, wn = warp / WM, g = lane >> 2, tq = lane & 3;
 
     auto load = [&](int stage, int kt) {
         const int kb = k0 + kt * KB;
@@ -132,9 +137,9 @@ screen_product_mma(const double* __restrict__ tab, const double* __restrict__ in
         else cp_async_commit();
     }
 
-    double acc[4][NTW][2];
+    double acc[WMT][NTW][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < WMT; ++i)
 #pragma unroll
         for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -144,17 +149,17 @@ screen_product_mma(const double* __restrict__ tab, const double* __restrict__ in
         const int nx = kt + STAGES - 1;
         if (nx < nk) load(nx % STAGES, nx);
         else cp_async_commit();
-        const double* ps = Ps + (kt % STAGES) * ROWS * MPP + (wm * 32 + g) * MPP + tq;
+        const double* ps = Ps + (kt % STAGES) * ROWS * MPP + (wm * 8 * WMT + g) * MPP + tq;
         const double* is = Is + (kt % STAGES) * KB * TP + tq * TP + wn * NTW * 8 + g;
 #pragma unroll
         for (int kk = 0; kk < KB; kk += 4) {
-            double a[4], b[NTW];
+            double a[WMT], b[NTW];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = ps[i * 8 * MPP + kk];
+            for (int i = 0; i < WMT; ++i) a[i] = ps[i * 8 * MPP + kk];
 #pragma unroll
             for (int j = 0; j < NTW; ++j) b[j] = is[kk * TP + j * 8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < WMT; ++i)
 #pragma unroll
                 for (int j = 0; j < NTW; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
@@ -163,8 +168,8 @@ screen_product_mma(const double* __restrict__ tab, const double* __restrict__ in
 
     double* out = part + ((size_t)split * NT + tb) * L * TP;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int row = row0 + wm * 32 + i * 8 + g;
+    for (int i = 0; i < WMT; ++i) {
+        const int row = row0 + wm * 8 * WMT + i * 8 + g;
         if (row < L) {
 #pragma unroll
             for (int j = 0; j < NTW; ++j)
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(256) dmma_peak(double* sink, int iters) {
 template <int NTW>
 void launch_mma(dim3 grid, int wn, cudaStream_t s, const double* tab, const double* inj,
                 double* part, int L, int Bp, int NT, int kper) {
-    screen_product_mma<NTW><<<grid, 128 * wn, mma_smem(NTW, wn), s>>>(tab, inj, part, L, Bp, NT,
+    screen_product_mma<NTW><<<grid, 32 * WM * wn, mma_smem(NTW, wn), s>>>(tab, inj, part, L, Bp, NT,
                                                                       kper, wn);
 }
 using MmaFn = void (*)(dim3, int, cudaStream_t, const double*, const double*, double*, int, int,
@@ -281,7 +286,7 @@ struct hpr_screen {
     // bus splits: row tiles x S x NT should fill whole waves of resident CTAs
     void plan() {
         int per_sm = 0;
-        SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kMmaFns[NTW - 1], 128 * WN,
+        SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kMmaFns[NTW - 1], 32 * WM * WN,
                                                           mma_smem(NTW, WN)));
         if (per_sm < 1) fail(HPR_ERR_CUDA, "screen product kernel does not fit on an SM");
         ctas = per_sm;
