@@ -399,6 +399,8 @@ extern "C" int hpr_screen_run(hpr_screen* h, const double* injections, int32_t n
     h->WN = (tiles + NTW_MAX - 1) / NTW_MAX;
     h->NTW = (tiles + h->WN - 1) / h->WN;
     h->Tp = h->WN * h->NTW * 8;
+    if (32 * WM * h->WN > 256)
+        fail(HPR_ERR_INVALID, "hpr_screen_run: too many periods for this build's warp tile");
     h->tol = tol;
     h->plan();
     h->grow(h->inj, h->inj_cap, (size_t)h->Bp * h->Tp);
