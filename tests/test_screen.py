@@ -314,3 +314,21 @@ def test_fp64_peak_probe_is_plausible():
     """The measured DMMA ceiling the bench's screen roofline divides by."""
     v = screen.fp64_peak_tflops()
     assert 5.0 < v < 100.0
+
+
+@pytest.mark.gpu
+def test_nonfinite_point_matches_oracle():
+    """A NaN or inf in the point makes that period's flows non-finite; as in
+    the reference, NaN excesses never pass the test and +inf ones do."""
+    g = golden()
+    doc, inst, ptdf, tol = case(g, 0)
+    keys = inst.contingency_keys()
+    u, pp, pen, _ = screen.column_blocks(inst)
+    for bad in (np.nan, np.inf):
+        x = g["c0_p0_x"].copy()
+        x[pp[0, 3]] = bad
+        got = screen.screen_violations(x, inst, ptdf, tol=tol)
+        want = screen_oracle.screen(g["c0_tables"], g["c0_limits"], keys,
+                                    [ln.lid for ln in inst.lines], oracle_inj(doc, inst, x), (), tol)
+        assert {v.triple for v in got} == {w[:3] for w in want}
+        assert not any(v.period == 3 for v in got) or bad == np.inf
