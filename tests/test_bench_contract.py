@@ -39,6 +39,11 @@ def test_bench_line_has_the_contract_keys():
     assert e["status"] == "optimal-tolerance"
     assert d["gpu_launches"] > 0
     assert d["clocks"]["samples"] > 0 and "reasons" in d["clocks"]
+    sc = d["screen"]                  # flow-screen leg
+    assert "error" not in sc, sc
+    assert sc["product_us"] > 0 and sc["oracle_set_diff"] == 0 and sc["same_as_first"]
+    assert sc["roofline"]["bound"] == "fp64" and 0 < sc["roofline"]["frac"] < 1.2
+    assert sc["cpu_baseline"]["value"] > 0
 
 
 def test_reference_arm_line():
