@@ -171,10 +171,19 @@ def workload(args):
             f"SCUC LP relaxation + {tri}")
 
 
+def config_dict(args, m, n, nnz, ws, partitioned):
+    """The `config` object both arms print (identical, so the driver's
+    same-config check holds); per-arm details live outside it."""
+    return {"workload": workload(args), "rows": int(m), "cols": int(n), "nnz": int(nnz),
+            "l2": "inputs larger than L2 (matrix stream > 1 GB/iteration)",
+            "parallelism": (f"rowpart{ws}" if partitioned else
+                            (f"replicas{ws}" if ws > 1 else "single"))}
+
+
 def build_lp(args, device):
     from paper_2510_10891_b200 import scuc
     t = time.perf_counter()
-    doc, mon, lpa = scuc.build_config(args.config, n_triples=args.triples, device=device)
+    doc, mon, lpa = scuc.build_config(args.config, n_triples=args.triples)
     return lpa, time.perf_counter() - t, doc
 
 
@@ -373,18 +382,15 @@ def run_b200(args):
         "higher_is_better": True, "scaling": "strong" if partitioned else "weak",
         "vs_baseline": None,
         "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
-        "config": {"workload": workload(args),
-                   "rows": m, "cols": n, "nnz": nnz, "step": "16 HPR iterations + KKT check",
-                   "device_layout": {"folded_rows": lay["folded_rows"],
-                                     "folded_nnz": lay["folded_nnz"],
-                                     "f_nnz": lay["f_nnz"], "ft_nnz": lay["ft_nnz"],
-                                     "panel_nnz": lay["panel_nnz"],
-                                     "index_free_nnz_f": lay["index_free_nnz_f"],
-                                     "reordered": bool(lay["reordered"]),
-                                     "twin_folded": bool(lay["folded"])},
-                   "l2": "inputs larger than L2 (matrix stream > 1 GB/iteration)",
-                   "parallelism": (f"rowpart{ws}" if partitioned else
-                                   (f"replicas{ws}" if ws > 1 else "single"))},
+        "config": config_dict(args, m, n, nnz, ws, partitioned),
+        "step": "16 HPR iterations + KKT check",
+        "device_layout": {"folded_rows": lay["folded_rows"],
+                          "folded_nnz": lay["folded_nnz"],
+                          "f_nnz": lay["f_nnz"], "ft_nnz": lay["ft_nnz"],
+                          "panel_nnz": lay["panel_nnz"],
+                          "index_free_nnz_f": lay["index_free_nnz_f"],
+                          "reordered": bool(lay["reordered"]),
+                          "twin_folded": bool(lay["folded"])},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                      "bytes_per_launch": dom_b, "seconds_per_launch": dom_t,
@@ -415,7 +421,7 @@ def run_b200(args):
     out["clocks"] = clk.summary()
 
     if partitioned:
-        out["config"]["block"] = {"rows": int(blk.rows.size), "nnz": int(blk.nnz)}
+        out["block"] = {"rows": int(blk.rows.size), "nnz": int(blk.nnz)}
     x_point = np.zeros(n)
     if not args.no_e2e and not partitioned:
         # public API from host buffers: upload + setup + solve to 1e-4 + copy back.
@@ -525,9 +531,8 @@ def run_reference(args):
            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
            "data": "synthetic",
-           "config": {"workload": workload(args),
-                      "rows": m, "cols": n, "nnz": lpa.nnz,
-                      "step": "1 HPR iteration (KKT check every 16th)"},
+           "config": config_dict(args, m, n, lpa.nnz, ws, args.mode == "partitioned"),
+           "step": "1 HPR iteration (KKT check every 16th)",
            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "port",
                             "sample": f"{args.steps} iterations after {args.warmup} warm-up "
                                       f"(oracle setup {t_setup:.1f} s untimed; scipy SpMV "

@@ -85,6 +85,11 @@ struct Ctrl {
     int has_deadline;
     int status;                   // -1 running, else HPR_* status
     int flag_improved, flag_restart;
+    // sigma update at a restart (hprlp.py:437-441): the device forms the
+    // ratio, the host applies ratio ** damping with the C library's pow --
+    // the function Python's float ** calls -- and relaunches the loop
+    int sigma_pending;
+    double sigma_ratio;
     long long checks;
     // logging
     long long n_log, log_cap;

@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "hpr_common.cuh"
+#include "hpr_device_scope.h"
 #include "hpr_setup.cuh"
 #include "hpr_spmv.cuh"
 #include "hpr_update.cuh"
@@ -867,6 +868,8 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
 // Partitioned mode: one block per launch; every rank reads the (identical)
 // controller status, and the wall-clock limit is agreed by a MAX all-reduce so
 // no rank leaves the collective sequence alone.
+bool host_sigma_update(hpr_handle* h);
+
 double run_loop_partitioned(hpr_handle* h, double time_left) {
     cudaStream_t s = h->stream;
     const auto t0 = std::chrono::steady_clock::now();
@@ -884,6 +887,7 @@ double run_loop_partitioned(hpr_handle* h, double time_left) {
         CK(cudaStreamSynchronize(s));
         std::memcpy(&flag, &h->h_scal[0], sizeof(int));
         if (h->h_ctrl->status != -1) break;
+        host_sigma_update(h);            // replicated controller: same ratio on every rank
         if (flag) {
             h->h_ctrl->status = HPR_TIME_LIMIT;
             CK(cudaMemcpyAsync(&h->ctrl->status, &h->h_ctrl->status, sizeof(int),
@@ -899,8 +903,37 @@ double run_loop_partitioned(hpr_handle* h, double time_left) {
     return ms * 1e-3;
 }
 
+// The restart's sigma update (hprlp.py:437-441) as Python evaluates it:
+// float(np.clip(ratio ** damping, 0.25, 4.0)) with ratio from the device
+// controller; Python's float ** calls the C library's pow, so this is the
+// same function on the same bits.  The controller stopped the loop at the
+// restart's check; returns true when the loop must be relaunched.
+bool host_sigma_update(hpr_handle* h) {
+    Ctrl& c = *h->h_ctrl;
+    if (c.status != -1 || !c.sigma_pending) return false;
+    double f = std::pow(c.sigma_ratio, c.damping);
+    if (!(f >= 0.25) && f == f) f = 0.25;           // np.clip: NaN passes through
+    if (!(f <= 4.0) && f == f) f = 4.0;
+    c.sigma = c.sigma * f;
+    c.sigma_pending = 0;
+    cudaStream_t s = h->stream;
+    CK(cudaMemcpyAsync(&h->ctrl->sigma, &c.sigma, sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&h->ctrl->sigma_pending, &c.sigma_pending, sizeof(int),
+                       cudaMemcpyHostToDevice, s));
+    return true;
+}
+
+double run_loop_once(hpr_handle* h);
+
 double run_loop(hpr_handle* h, double time_left = -1.0) {
     if (h->comm || plain_graph()) return run_loop_partitioned(h, time_left);
+    double secs = 0.0;
+    do secs += run_loop_once(h);
+    while (host_sigma_update(h));
+    return secs;
+}
+
+double run_loop_once(hpr_handle* h) {
     cudaStream_t s = h->stream;
     unsigned long long cv = h->gcond;
     CK(cudaMemcpyAsync(&h->ctrl->cond, &cv, sizeof(cv), cudaMemcpyHostToDevice, s));
@@ -954,6 +987,7 @@ double run_eager(hpr_handle* h, int B) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
         total += ms;
+        host_sigma_update(h);
     } while (h->h_ctrl->status == -1);
     return total * 1e-3;
 }
@@ -1241,7 +1275,8 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             h->world = std::max(1, opt->world_size);
             h->rank = opt->rank;
         }
-        CK(cudaSetDevice(h->dev));
+        hpr::DeviceScope dscope_(h->dev);
+        CK(dscope_.err);
         h->m = p->m;
         h->n = p->n;
         h->n_eq = p->n_eq;
@@ -1567,7 +1602,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
 
 void hpr_destroy(hpr_handle* h) {
     if (!h) return;
-    cudaSetDevice(h->dev);
+    hpr::DeviceScope dscope_(h->dev);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
     if (h->graph) cudaGraphDestroy(h->graph);
@@ -1597,7 +1632,8 @@ int hpr_solve(hpr_handle* h, const hpr_params* prm, const double* x0, const doub
     const auto t0 = std::chrono::steady_clock::now();
     if (!h || !stats) fail(HPR_ERR_INVALID, "handle/stats is NULL");
     check_params(prm);
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     std::memset(stats, 0, sizeof(*stats));
     h->launches = 0;
     if (prm->precision == HPR_FP32)
@@ -1621,7 +1657,8 @@ int hpr_get_log(hpr_handle* h, hpr_log_record* out, int64_t cap, int64_t* n_out)
 int hpr_matvec(hpr_handle* h, int32_t transpose, const double* in, double* out) {
     API_BEGIN
     if (!h || !in || !out) fail(HPR_ERR_INVALID, "NULL argument");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     const DevCsr& M = transpose ? h->AT : h->A;
     const int nin = transpose ? h->m : h->n, nout = transpose ? h->n : h->m;
     double* xin = transpose ? h->YM : h->XM;   // master scratch of the input length
@@ -1638,7 +1675,8 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
                      hpr_kkt* out) {
     API_BEGIN
     if (!h || !x || !y || !z || !out) fail(HPR_ERR_INVALID, "NULL argument");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     cudaStream_t s = h->stream;
     put_vec(h, h->XM, x, h->n, false);
     put_vec(h, h->YM, y, h->m, true);
@@ -1683,7 +1721,8 @@ int hpr_power_method(hpr_handle* h, double tol, int32_t max_iter, double inflati
                      int32_t* converged) {
     API_BEGIN
     if (!h || !lam) fail(HPR_ERR_INVALID, "NULL argument");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     int it = 0, cv = 0;
     *lam = power_method(h, h->A.mval, h->AT.mval, tol, max_iter, inflation, start, start_count,
                         &it, &cv);
@@ -1699,7 +1738,8 @@ int hpr_iterate(hpr_handle* h, int32_t precision, double sigma, double lam, int6
     API_BEGIN
     if (!h || !x || !y || !z || !ax || !ay || !az) fail(HPR_ERR_INVALID, "NULL argument");
     if (precision != HPR_FP64 && precision != HPR_FP32) fail(HPR_ERR_INVALID, "unknown precision");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     cudaStream_t s = h->stream;
     const int m = h->m, n = h->n;
     const bool fp32 = precision == HPR_FP32;
@@ -1795,7 +1835,8 @@ int hpr_nccl_comm_init(const uint8_t id[128], int32_t world_size, int32_t rank, 
     API_BEGIN
     if (!id || !comm_out || world_size < 1 || rank < 0 || rank >= world_size)
         fail(HPR_ERR_INVALID, "bad argument");
-    CK(cudaSetDevice(device));
+    hpr::DeviceScope dscope_(device);
+    CK(dscope_.err);
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     ncclComm_t comm;
@@ -1839,7 +1880,8 @@ int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_sta
     if (!h || !st) fail(HPR_ERR_INVALID, "NULL argument");
     if (h->last_prec < 0 || (!h->gexec && !use_eager(h, h->h_ctrl->B)))
         fail(HPR_ERR_INVALID, "hpr_resume needs a prior looping solve");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     std::memset(st, 0, sizeof(*st));
     h->launches = 0;
     read_ctrl(h);
@@ -1875,7 +1917,8 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
     if (which < 0 || which > 6) fail(HPR_ERR_INVALID, "unknown kernel");
-    CK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    CK(dscope_.err);
     cudaStream_t s = h->stream;
     // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update,
     //        4 = one whole KKT check (2 master products, row/col terms, controller, copies;

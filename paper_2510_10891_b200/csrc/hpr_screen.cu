@@ -29,6 +29,8 @@
 
 #include <cuda_runtime.h>
 
+#include "hpr_device_scope.h"
+
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -347,7 +349,8 @@ extern "C" int hpr_screen_create(int32_t device, int32_t n_lines, int32_t n_buse
     *out = nullptr;
     if (n_lines <= 0 || n_buses <= 0 || n_tables <= 0)
         fail(HPR_ERR_EMPTY, "hpr_screen_create: empty PTDF table set");
-    SCK(cudaSetDevice(device));
+    hpr::DeviceScope dscope_(device);
+    SCK(dscope_.err);
     auto* h = new hpr_screen();
     try {
         h->dev = device;
@@ -393,7 +396,8 @@ extern "C" int hpr_screen_run(hpr_screen* h, const double* injections, int32_t n
     if (n_periods <= 0) fail(HPR_ERR_EMPTY, "hpr_screen_run: no periods");
     if (n_periods > 2 * NTW_MAX * 8)
         fail(HPR_ERR_INVALID, "hpr_screen_run: more than 96 periods per screen");
-    SCK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    SCK(dscope_.err);
     h->T = n_periods;
     const int tiles = (n_periods + 7) / 8;
     h->WN = (tiles + NTW_MAX - 1) / NTW_MAX;
@@ -434,7 +438,8 @@ extern "C" int hpr_screen_fetch(hpr_screen* h, int32_t* table, int32_t* line, in
                                 double* flow, double* excess) {
     SCREEN_API_BEGIN
     if (!h) fail(HPR_ERR_INVALID, "hpr_screen_fetch: null handle");
-    SCK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    SCK(dscope_.err);
     const size_t n = (size_t)h->found;
     if (n) {
         if (table) SCK(cudaMemcpyAsync(table, h->r_tab, n * 4, cudaMemcpyDefault, h->stream));
@@ -452,7 +457,8 @@ extern "C" int hpr_screen_flows(hpr_screen* h, int32_t table, double* flows) {
     if (!h || !flows) fail(HPR_ERR_INVALID, "hpr_screen_flows: null argument");
     if (h->T == 0) fail(HPR_ERR_INVALID, "hpr_screen_flows: no screen has run");
     if (table < 0 || table >= h->NT) fail(HPR_ERR_INVALID, "hpr_screen_flows: table out of range");
-    SCK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    SCK(dscope_.err);
     const size_t per = (size_t)h->L * h->T;
     SCK(cudaMemcpyAsync(flows, h->flows + per * table, per * sizeof(double), cudaMemcpyDefault,
                         h->stream));
@@ -465,7 +471,8 @@ extern "C" int hpr_screen_bench(hpr_screen* h, int32_t reps, double* us_product,
     SCREEN_API_BEGIN
     if (!h || reps <= 0) fail(HPR_ERR_INVALID, "hpr_screen_bench: bad argument");
     if (h->T == 0) fail(HPR_ERR_INVALID, "hpr_screen_bench: no screen has run");
-    SCK(cudaSetDevice(h->dev));
+    hpr::DeviceScope dscope_(h->dev);
+    SCK(dscope_.err);
     h->launch();  // warm
     h->epilogue();
     SCK(cudaEventRecord(h->ev[0], h->stream));
@@ -498,7 +505,8 @@ extern "C" int hpr_screen_info_get(hpr_screen* h, hpr_screen_info* info) {
 extern "C" int hpr_fp64_peak_bench(int32_t device, double* tflops) {
     SCREEN_API_BEGIN
     if (!tflops) fail(HPR_ERR_INVALID, "hpr_fp64_peak_bench: null argument");
-    SCK(cudaSetDevice(device));
+    hpr::DeviceScope dscope_(device);
+    SCK(dscope_.err);
     int sms = 0;
     SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     double* sink = nullptr;
@@ -525,6 +533,6 @@ extern "C" int hpr_fp64_peak_bench(int32_t device, double* tflops) {
 
 extern "C" void hpr_screen_destroy(hpr_screen* h) {
     if (!h) return;
-    cudaSetDevice(h->dev);
+    hpr::DeviceScope dscope_(h->dev);
     delete h;
 }

@@ -377,10 +377,11 @@ k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int 
         if (suff || stalled) {
             const double dx = sqrt(s_dx), dy = sqrt(s_dy);       // :437-441
             if (dx > 1e-14 && dy > 1e-14 && c->norm_a > 0) {
-                const double ratio = dx / (c->norm_a * dy * c->sigma);
-                double f = c->damping == 0.5 ? sqrt(ratio) : pow(ratio, c->damping);
-                f = np_min(np_max(f, 0.25), 4.0);
-                c->sigma = c->sigma * f;
+                // sigma *= clip(ratio ** damping, 1/4, 4) is applied by the host
+                // (host_sigma_update): CUDA's pow is not the C library's, and
+                // even pow(r, 0.5) != sqrt(r) for ~0.08% of r under glibc
+                c->sigma_ratio = dx / (c->norm_a * dy * c->sigma);
+                c->sigma_pending = 1;
             }
             restart = 1;                                       // :442-446
             c->k0 = 0;
@@ -401,7 +402,8 @@ k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int 
         if (tnow + c->B > c->max_iter) c->status = HPR_ITERATION_LIMIT;
         else if (c->has_deadline && globaltimer() > c->deadline_ns) c->status = HPR_TIME_LIMIT;
     }
-    if (c->cond) cudaGraphSetConditional(c->cond, c->status == -1 ? 1u : 0u);
+    if (c->cond)
+        cudaGraphSetConditional(c->cond, (c->status == -1 && !c->sigma_pending) ? 1u : 0u);
 }
 
 // best-triple save and restart copies (hprlp.py:172-181, 422-424, 430)

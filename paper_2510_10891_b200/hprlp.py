@@ -461,9 +461,9 @@ def power_method(lp_or_matrix, tol=1e-4, max_iter=1000, seed=0, inflation=None) 
     return lam
 
 
-def _solve_once(lp, config, start, t_start):
-    eng = engine_for(lp)
-    x, y, z, st, recs = eng.solve_raw(config, start, time.perf_counter() - t_start)
+def _assemble(lp, config, x, y, z, st, recs, t_start, stats):
+    """A SolveResult (hprlp.py:448-455) from one device solve: best triple,
+    status, KKT of the returned point, and both logs (hprlp.py:412-420)."""
     status = getattr(_CLS.status, _STATUS_BY_CODE[st.status])
     residual_log, rate_log = [], []
     if config.log_every_iteration:
@@ -479,9 +479,6 @@ def _solve_once(lp, config, start, t_start):
                       solve_time=time.perf_counter() - t_start, sigma_final=st.sigma_final,
                       lam=st.lam, residual_log=residual_log, rate_log=rate_log,
                       precision_used=_precision_member(_precision_value(config.precision)))
-    stats = {"setup_seconds": st.setup_seconds, "loop_seconds": st.loop_seconds,
-             "gpu_launches": int(st.gpu_launches), "power_iterations": st.power_iterations,
-             "checks": int(st.checks), "device_objective": st.objective}
     try:
         res.device_stats = stats
     except AttributeError:
@@ -489,20 +486,34 @@ def _solve_once(lp, config, start, t_start):
     return res
 
 
-def solve(lp, config=None, start=None):
-    """``hprlp.solve`` (hprlp.py:319-329) on the GPU: one device solve, and an
-    FP64 retry when an FP32 solve loses finiteness."""
-    config = config or SolverConfig()
-    t_start = time.perf_counter()
-    result = _solve_once(lp, config, start, t_start)
+def _solve_once(lp, config, start, t_start, engine=None):
+    eng = engine_for(lp) if engine is None else engine
+    x, y, z, st, recs = eng.solve_raw(config, start, time.perf_counter() - t_start)
+    stats = {"setup_seconds": st.setup_seconds, "loop_seconds": st.loop_seconds,
+             "gpu_launches": int(st.gpu_launches), "power_iterations": st.power_iterations,
+             "checks": int(st.checks), "device_objective": st.objective}
+    return _assemble(lp, config, x, y, z, st, recs, t_start, stats)
+
+
+def _with_fp64_retry(config, run):
+    """``solve``'s FP32 -> FP64 retry (hprlp.py:324-328): `run(cfg, t_start)`
+    is one solve; an FP32 numerical failure reruns it in FP64."""
+    result = run(config, time.perf_counter())
     if (result.status.value == "numerical-failure"
             and _precision_value(config.precision) == "fp32"):
         log.warning("FP32 solve failed numerically; retrying in FP64")
         cfg64 = replace(config, precision=type(config.precision)("fp64")) \
             if hasattr(config, "__dataclass_fields__") else config
-        result = _solve_once(lp, cfg64, start, time.perf_counter())
+        result = run(cfg64, time.perf_counter())
         result.fp64_fallback = True
     return result
+
+
+def solve(lp, config=None, start=None):
+    """``hprlp.solve`` (hprlp.py:319-329) on the GPU: one device solve, and an
+    FP64 retry when an FP32 solve loses finiteness."""
+    return _with_fp64_retry(config or SolverConfig(),
+                            lambda cfg, t0: _solve_once(lp, cfg, start, t0))
 
 
 def solve_many(lps, config=None, starts=None, workers: int | None = None) -> list:
@@ -524,9 +535,25 @@ def solve_many(lps, config=None, starts=None, workers: int | None = None) -> lis
         raise ValueError("starts must match lps")
     if not lps:
         return []
+    import torch
+    config = config or SolverConfig()
+    dev = torch.cuda.current_device()
     workers = max(1, min(workers or 8, len(lps)))
+
+    def one(a):
+        # a private engine per entry: two entries never share a handle (a
+        # handle is not thread-safe), and the caller's device, not the
+        # worker thread's default 0, holds it
+        torch.cuda.set_device(dev)
+        eng = Engine(a[0], device=dev)
+        try:
+            return _with_fp64_retry(config,
+                                    lambda cfg, t0: _solve_once(a[0], cfg, a[1], t0, engine=eng))
+        finally:
+            eng.close()
+
     with ThreadPoolExecutor(max_workers=workers) as ex:
-        return list(ex.map(lambda a: solve(a[0], config, a[1]), zip(lps, starts)))
+        return list(ex.map(one, zip(lps, starts)))
 
 
 def write_iteration_log(path, result, solve_id: str = "solve") -> None:
@@ -582,11 +609,11 @@ def solve_partitioned(lp, config=None, start=None, comm: NcclComm | None = None,
     """``solve`` with A row-partitioned over the ranks of `group` (one GPU per
     rank).  Every rank passes the same full LP; each keeps its row block
     (paper_2510_10891_b200.partition).  x, z come back replicated and y is
-    gathered, so every rank returns the full SolveResult."""
+    gathered, so every rank returns the full SolveResult -- with the same
+    logs and the same FP32 -> FP64 retry as :func:`solve` (the retry decision
+    is taken on replicated controller state, so all ranks take it together)."""
     import torch.distributed as dist
     from . import partition
-    config = config or SolverConfig()
-    t_start = time.perf_counter()
     own = comm is None
     comm = comm or NcclComm(group)
     try:
@@ -600,34 +627,27 @@ def solve_partitioned(lp, config=None, start=None, comm: NcclComm | None = None,
         if start is not None:
             y0 = np.broadcast_to(np.asarray(start[1], dtype=np.float64), (csr.shape[0],))
             sub_start = (start[0], y0[blk.rows], start[2])
-        x, yb, z, st, recs = eng.solve_raw(config, sub_start, time.perf_counter() - t_start,
-                                           rows=blk.rows, m_total=csr.shape[0])
-        parts = [None] * comm.world_size
-        dist.all_gather_object(parts, (blk.rows, yb), group=group)
-        y = np.empty(csr.shape[0])
-        for rows, yy in parts:
-            y[rows] = yy
-        eng.close()
+
+        def run(cfg, t_start):
+            x, yb, z, st, recs = eng.solve_raw(cfg, sub_start, time.perf_counter() - t_start,
+                                               rows=blk.rows, m_total=csr.shape[0])
+            parts = [None] * comm.world_size
+            dist.all_gather_object(parts, (blk.rows, yb), group=group)
+            y = np.empty(csr.shape[0])
+            for rows, yy in parts:
+                y[rows] = yy
+            stats = {"loop_seconds": st.loop_seconds, "gpu_launches": int(st.gpu_launches),
+                     "world_size": comm.world_size, "block_rows": int(blk.rows.size),
+                     "block_nnz": int(blk.nnz)}
+            return _assemble(lp, cfg, x, y, z, st, recs, t_start, stats)
+
+        try:
+            return _with_fp64_retry(config or SolverConfig(), run)
+        finally:
+            eng.close()
     finally:
         if own:
             comm.close()
-    status = getattr(_CLS.status, _STATUS_BY_CODE[st.status])
-    residual_log = [{"iteration": r.iteration, "epoch": r.epoch, "rel_primal": r.rel_primal,
-                     "rel_dual": r.rel_dual, "rel_box": r.rel_box, "rel_gap": r.rel_gap,
-                     "sigma": r.sigma} for r in recs] if config.log_residuals else []
-    objective = float(np.dot(_f64(lp.cost), x)) + float(getattr(lp, "offset", 0.0))
-    res = _CLS.result(x=x, y=y, z=z, status=status, objective=objective, kkt=_kkt_obj(st.kkt),
-                      iterations=int(st.iterations), restarts=int(st.restarts),
-                      solve_time=time.perf_counter() - t_start, sigma_final=st.sigma_final,
-                      lam=st.lam, residual_log=residual_log,
-                      precision_used=_precision_member(_precision_value(config.precision)))
-    try:
-        res.device_stats = {"loop_seconds": st.loop_seconds, "gpu_launches": int(st.gpu_launches),
-                            "world_size": comm.world_size, "block_rows": int(blk.rows.size),
-                            "block_nnz": int(blk.nnz)}
-    except AttributeError:
-        pass
-    return res
 
 
 # ---------------------------------------------------------------------------

@@ -100,14 +100,14 @@ class FlowScreen:
 
     def __init__(self, ptdf, keys, lines, device: int = 0):
         self.lib = _capi.load()
+        self.device = int(device)
         self.keys = list(keys)
         self.line_ids = [ln.lid for ln in lines]
         tabs = [np.ascontiguousarray(ptdf.table(k), dtype=np.float64) for k in self.keys]
         n_l, n_b = tabs[0].shape
         if n_l != len(self.line_ids):
             raise ValueError("PTDF rows do not match the instance's lines")
-        self.limits = np.ascontiguousarray(
-            [[ln.limit_for(k) for ln in lines] for k in self.keys], dtype=np.float64)
+        self.limits = limit_table(types.SimpleNamespace(lines=lines), self.keys)
         self.shape = (n_l, n_b)
         self.line_rank = _ranks(self.line_ids)
         self.key_rank = _ranks(self.keys)
@@ -120,11 +120,22 @@ class FlowScreen:
         self._fin = weakref.finalize(self, self.lib.hpr_screen_destroy, h)
 
     def close(self):
+        """Free the device tables; the object (and any cache entry holding
+        it) is dead afterwards -- every later call raises."""
         self._fin()
+        self.handle = None
+        for key, ent in list(_SCREENS.items()):
+            if ent[1] is self:
+                _SCREENS.pop(key, None)
+
+    def _h(self):
+        if self.handle is None:
+            raise ValueError("FlowScreen is closed")
+        return self.handle
 
     def info(self) -> dict:
         info = _capi.ScreenInfo()
-        _capi.check(self.lib.hpr_screen_info_get(self.handle, C.byref(info)))
+        _capi.check(self.lib.hpr_screen_info_get(self._h(), C.byref(info)))
         return {k: getattr(info, k) for k, _ in info._fields_}
 
     def run(self, inj: np.ndarray, tol: float):
@@ -140,12 +151,12 @@ class FlowScreen:
         for t0 in range(0, max(n_t, 1), PERIODS_PER_LAUNCH):
             chunk = np.ascontiguousarray(inj[:, t0:t0 + PERIODS_PER_LAUNCH])
             n = C.c_int64()
-            _capi.check(self.lib.hpr_screen_run(self.handle, _capi.ptr(chunk), chunk.shape[1],
+            _capi.check(self.lib.hpr_screen_run(self._h(), _capi.ptr(chunk), chunk.shape[1],
                                                 float(tol), C.byref(n)))
             k = n.value
             rec = (np.empty(k, np.int32), np.empty(k, np.int32), np.empty(k, np.int32),
                    np.empty(k, np.float64), np.empty(k, np.float64))
-            _capi.check(self.lib.hpr_screen_fetch(self.handle, *[_capi.ptr(a) for a in rec]))
+            _capi.check(self.lib.hpr_screen_fetch(self._h(), *[_capi.ptr(a) for a in rec]))
             rec[2][:] += t0
             parts.append(rec)
         self._last_t = n_t if n_t <= PERIODS_PER_LAUNCH else -1
@@ -159,12 +170,12 @@ class FlowScreen:
         if self._last_t < 0:
             raise ValueError("flows() holds only the last period chunk of a long horizon")
         out = np.empty((self.shape[0], self._last_t), np.float64)
-        _capi.check(self.lib.hpr_screen_flows(self.handle, table, _capi.ptr(out)))
+        _capi.check(self.lib.hpr_screen_flows(self._h(), table, _capi.ptr(out)))
         return out
 
     def bench(self, reps: int = 20) -> tuple:
         a, b = C.c_double(), C.c_double()
-        _capi.check(self.lib.hpr_screen_bench(self.handle, reps, C.byref(a), C.byref(b)))
+        _capi.check(self.lib.hpr_screen_bench(self._h(), reps, C.byref(a), C.byref(b)))
         return a.value, b.value
 
 
@@ -221,18 +232,36 @@ def fp64_peak_tflops(device: int = 0) -> float:
 _SCREENS: dict = {}
 
 
-def screen_for(ptdf, instance, device: int = 0, keys=None) -> FlowScreen:
+def limit_table(instance, keys) -> np.ndarray:
+    """(len(keys) x n_lines) limits, ``Line.limit_for`` (instance.py:88-89):
+    the normal limit for the base case, the emergency limit otherwise --
+    one pass over the lines, then a broadcast over the keys."""
+    lines = instance.lines
+    base = np.array([ln.limit_for("base") for ln in lines], dtype=np.float64)
+    cont = [k for k in keys if k != "base"]
+    emer = (np.array([ln.limit_for(cont[0]) for ln in lines], dtype=np.float64)
+            if cont else base)
+    is_base = np.array([k == "base" for k in keys], dtype=bool)
+    return np.ascontiguousarray(np.where(is_base[:, None], base[None, :], emer[None, :]))
+
+
+def screen_for(ptdf, instance, device: int | None = None, keys=None) -> FlowScreen:
     """The resident screen of ``ptdf`` (built once; ``PtdfTable`` is
-    immutable, ``instance.py:141-147``), rebuilt only if the instance's keys
-    or limits differ from the ones it was built with.  ``keys`` restricts the
-    resident tables to a subset of the instance's keys (one rank's shard)."""
+    immutable, ``instance.py:141-147``) on `device` (default: the caller's
+    current CUDA device), rebuilt only if the device, the instance's keys or
+    its limits differ from the ones it was built with.  ``keys`` restricts
+    the resident tables to a subset of the instance's keys (one rank's
+    shard)."""
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
     keys = list(instance.contingency_keys() if keys is None else keys)
     ent = _SCREENS.get(id(ptdf))
     if ent is not None:
         ref, scr = ent
-        if ref() is ptdf and scr.keys == keys and scr.line_ids == [ln.lid for ln in instance.lines]:
-            lim = np.array([[ln.limit_for(k) for ln in instance.lines] for k in keys])
-            if np.array_equal(lim, scr.limits):
+        if (ref() is ptdf and scr.handle is not None and scr.device == int(device)
+                and scr.keys == keys and scr.line_ids == [ln.lid for ln in instance.lines]):
+            if np.array_equal(limit_table(instance, keys), scr.limits):
                 return scr
         scr.close()
     scr = FlowScreen(ptdf, keys, instance.lines, device=device)
@@ -312,11 +341,12 @@ def screen_violations_sharded(point, instance, ptdf, monitored=(), tol: float = 
             import torch
             device = torch.cuda.current_device()
         local = screen_for(ptdf, instance, device=device, keys=mine).run(inj, tol)
-    pos = np.array([keys.index(k) for k in mine] or [0], dtype=np.int32)
+    where = {k: i for i, k in enumerate(keys)}
+    pos = np.array([where[k] for k in mine] or [0], dtype=np.int32)
     local = (pos[local[0]],) + tuple(local[1:])
     parts = [None] * ws
     dist.all_gather_object(parts, local, group=group)
     recs = tuple(np.concatenate([p[i] for p in parts]) for i in range(5))
     lids = [ln.lid for ln in instance.lines]
-    lim = np.array([[ln.limit_for(k) for ln in instance.lines] for k in keys], dtype=np.float64)
-    return _assemble(recs, keys, lids, lim, _ranks(lids), _ranks(keys), monitored)
+    return _assemble(recs, keys, lids, limit_table(instance, keys), _ranks(lids), _ranks(keys),
+                     monitored)

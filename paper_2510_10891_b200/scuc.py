@@ -259,6 +259,19 @@ class LpArrays:
 # PTDF rows
 # ---------------------------------------------------------------------------
 
+# Host PTDF solves run under a fixed-size BLAS thread pool.  OpenBLAS splits a
+# dense solve by thread count, so its last bits depend on it: with the pool
+# pinned, the build container (8 cores) and the B200 box (16 cores, same CPU
+# model) produce bit-identical PTDF rows, hence identical LPs (digests), which
+# is what lets the committed reference trajectories be replayed on the box.
+PTDF_BLAS_THREADS = 8
+
+
+def _blas_pool():
+    from threadpoolctl import threadpool_limits
+    return threadpool_limits(PTDF_BLAS_THREADS)
+
+
 def _ptdf_full_reference(n_b, fb, tb, react, ref, skip=None):
     """PTDF exactly as ``instance._ptdf_matrix`` computes it
     (``scuckit/instance.py:199-238``): dense solve of the reduced B-matrix
@@ -276,7 +289,8 @@ def _ptdf_full_reference(n_b, fb, tb, react, ref, skip=None):
         b_full[j, i] -= b
     keep = [i for i in range(n_b) if i != ref]
     b_red = b_full[np.ix_(keep, keep)]
-    theta_red = scipy.linalg.solve(b_red, np.eye(n_b - 1), assume_a="sym")
+    with _blas_pool():
+        theta_red = scipy.linalg.solve(b_red, np.eye(n_b - 1), assume_a="sym")
     theta = np.zeros((n_b, n_b))
     theta[np.ix_(keep, keep)] = theta_red
     delta = np.zeros((len(fb), n_b))
@@ -336,7 +350,8 @@ def _ptdf_rows_direct(n_b, fb, tb, react, ref, lines, skip=None, device=None):
                 rhs[pos[fb[k]], c] += 1.0
             if pos[tb[k]] >= 0:
                 rhs[pos[tb[k]], c] -= 1.0
-        w = scipy.linalg.solve(bred, rhs, assume_a="sym")
+        with _blas_pool():
+            w = scipy.linalg.solve(bred, rhs, assume_a="sym")
     out = np.zeros((len(lines), n_b))
     out[:, keep] = w.T
     out /= react[np.asarray(lines)][:, None]
@@ -677,7 +692,12 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
 def build_config(name: str, n_triples: int | None = None, ptdf_method: str | None = None,
                  device=None, seed: int | None = None):
     """Instance + LP for a named config.  C1 monitors all base triples by
-    default; C2-C4 draw `n_triples` base triples."""
+    default; C2-C4 draw `n_triples` base triples.
+
+    The PTDF rows are solved on the host under the pinned BLAS pool
+    (``PTDF_BLAS_THREADS``) unless `device` is given explicitly, so the LP is
+    bit-identical wherever it is built; tests/golden/*_trajectory.json and
+    c4_window.json carry the digests the GPU parity tests assert."""
     cfg = dict(CONFIGS[name])
     if seed is not None:
         cfg["seed"] = seed

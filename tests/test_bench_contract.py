@@ -20,8 +20,12 @@ def _line(args):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+_LINES = {}
+
+
 def test_bench_line_has_the_contract_keys():
     d = _line(["--config", "C1", "--steps", "4", "--warmup", "3"])
+    _LINES["b200"] = d
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
@@ -49,5 +53,8 @@ def test_bench_line_has_the_contract_keys():
 def test_reference_arm_line():
     d = _line(["--impl", "reference", "--config", "C1", "--steps", "3", "--warmup", "3"])
     assert d["impl"] == "reference" and d["value"] > 0
+    if "b200" in _LINES:               # the driver's same-config check across the two arms
+        assert d["config"] == _LINES["b200"]["config"]
+        assert (d["metric"], d["unit"]) == (_LINES["b200"]["metric"], _LINES["b200"]["unit"])
     assert d["cpu_baseline"]["kind"] == "port"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0

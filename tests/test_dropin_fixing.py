@@ -62,6 +62,22 @@ def _near_threshold(x, tau, tol=1e-6):
     return bool(np.any((np.abs(x - tau) < tol) | (np.abs(x - (1 - tau)) < tol)))
 
 
+def _assert_fixed_sets(recs, tau, got, want, what):
+    """The north-star fixed-set criterion: identical sets unless a relaxed
+    value lies within 1e-6 of a fixing threshold.  A skipped comparison is
+    reported (warning + stdout), never silent."""
+    import warnings
+    near = [i for i, r in enumerate(recs) if _near_threshold(r[3], tau)]
+    if near:
+        msg = (f"{what}: fixed-set assertion skipped -- round(s) {near} have a relaxed "
+               f"value within 1e-6 of tau={tau}")
+        print(msg)
+        warnings.warn(msg)
+        return False
+    assert got == want
+    return True
+
+
 def test_successive_fixing_gpu_matches_cpu():
     """Small instance: the reference loop twice on the box, CPU HPR vs GPU."""
     import scuckit.hprlp as ref_hprlp
@@ -79,8 +95,8 @@ def test_successive_fixing_gpu_matches_cpu():
     for (oc, ic, sc, xc), (og, ig, sg, xg) in zip(cpu_rec, gpu_rec):
         assert sc == sg == "optimal-tolerance"
         assert abs(og - oc) <= 1e-6 * abs(oc)
-    if not any(_near_threshold(r[3], 0.1) for r in cpu_rec):
-        assert gpu_fixed == cpu_fixed and gpu_err == cpu_err
+    _assert_fixed_sets(cpu_rec, 0.1, (gpu_fixed, gpu_err), (cpu_fixed, cpu_err),
+                       "30-bus GPU vs CPU")
 
 
 def test_successive_fixing_c1_against_reference_record():
@@ -104,5 +120,4 @@ def test_successive_fixing_c1_against_reference_record():
         assert sg == r["status"]
         assert abs(og - r["objective"]) <= 1e-6 * abs(r["objective"])
     want = {int(k): v for k, v in g["fixed"].items()}
-    if not any(_near_threshold(r[3], 0.1) for r in rec):
-        assert fixed == want and err == g["error"]
+    _assert_fixed_sets(rec, 0.1, (fixed, err), (want, g["error"]), "C1 vs reference record")

@@ -334,79 +334,7 @@ def test_c1_tol_1e6_numerical_failure_matches_reference(H):
     assert abs(r.objective - g["objective"]) <= 1e-9 * abs(g["objective"])
 
 
-def test_c1_against_reference_trajectory(H):
-    """C1 (118-bus, all base flow rows; 24,504 x 13,200, 1.87M nnz) to 1e-4,
-    against the reference's own FP64/FP32 runs (tests/golden/c1_trajectory.json,
-    ~217 s / 118 s on the CPU).  The LP is rebuilt on the box; if its digest
-    differs from the fixture's (a different BLAS could move the PTDF last bit)
-    the comparison falls back to the on-box oracle's first 2,000 iterations."""
-    from paper_2510_10891_b200 import scuc
-    from paper_2510_10891_b200.lp import Precision
-    g = golden_io.c1()
-    assert g is not None
-    doc, mon, lpa = scuc.build_config("C1")
-    lp = lpa.to_lp()
-    if lpa.digest() != g["digest"]:
-        cfg = dict(tolerance=1e-4, ruiz=False, max_iterations=2000, log_residuals=True)
-        ref = O.solve(lpa, O.OracleConfig(**cfg))
-        r = H.solve(lp, H.SolverConfig(**cfg))
-        assert r.lam == pytest.approx(ref.lam, rel=1e-12)
-        assert abs(r.objective - ref.objective) <= 1e-6 * abs(ref.objective)
-        return
-    for tag, prec in (("fp64", "fp64"), ("fp32", "fp32")):
-        gg = g[tag]
-        r = H.solve(lp, H.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(prec),
-                                       log_residuals=True))
-        assert r.status.value == gg["status"]
-        assert r.lam == pytest.approx(gg["lam"], rel=1e-12)
-        if prec == "fp64":
-            assert abs(r.iterations - gg["iterations"]) <= 0.01 * gg["iterations"]
-            assert abs(r.restarts - gg["restarts"]) <= 1
-            assert abs(r.objective - gg["objective"]) <= 1e-6 * abs(gg["objective"])
-            mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"],
-                              e["rel_box"], e["rel_gap"], e["sigma"]] for e in r.residual_log])
-            ref = np.array(gg["log"])
-            np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
-        else:
-            assert abs(r.objective - gg["objective"]) <= 1e-4 * abs(gg["objective"])
-
-
-def test_c2_against_reference_trajectory(H):
-    """C2 + 500 triples (75,904 x 82,416, 1.85M nnz) to 1e-4 against the
-    reference's FP64 run (tests/golden/c2_trajectory.json).  Its PTDF flow rows
-    (up to ~1,900 entries) are long enough for the padded index-free rows and
-    the A^T y flow panels, so this pins those layout paths to the reference
-    (C1's flow rows are below both thresholds)."""
-    from paper_2510_10891_b200 import scuc
-    g = golden_io.c2()
-    if g is None:
-        pytest.skip("c2_trajectory.json not generated")
-    doc, mon, lpa = scuc.build_config("C2", n_triples=500)
-    lp = lpa.to_lp()
-    eng = H.Engine(lp)
-    lay = eng.layout()
-    eng.close()
-    assert lay["panel_nnz"] > 0 and lay["f_nnz"] > lay["folded_nnz"]     # the paths are live
-    same_lp = lpa.digest() == g["digest"]
-    if not same_lp:
-        # the box's BLAS can move the PTDF's last bits: check the on-box oracle too
-        cfg = dict(tolerance=1e-4, ruiz=False, max_iterations=2000, log_residuals=True)
-        ref = O.solve(lpa, O.OracleConfig(**cfg))
-        r = H.solve(lp, H.SolverConfig(**cfg))
-        assert r.lam == pytest.approx(ref.lam, rel=1e-12)
-        assert abs(r.objective - ref.objective) <= 1e-6 * abs(ref.objective)
-    gg = g["fp64"]
-    r = H.solve(lp, H.SolverConfig(tolerance=1e-4, ruiz=False, log_residuals=True))
-    assert r.status.value == gg["status"]
-    assert r.lam == pytest.approx(gg["lam"], rel=1e-12 if same_lp else 1e-9)
-    assert abs(r.iterations - gg["iterations"]) <= 0.01 * gg["iterations"]
-    assert abs(r.restarts - gg["restarts"]) <= 1
-    assert abs(r.objective - gg["objective"]) <= 1e-6 * abs(gg["objective"])
-    if same_lp:
-        mine = np.array([[e["iteration"], e["epoch"], e["rel_primal"], e["rel_dual"],
-                          e["rel_box"], e["rel_gap"], e["sigma"]] for e in r.residual_log])
-        ref = np.array(gg["log"])
-        np.testing.assert_allclose(mine[:200], ref[:200], rtol=1e-6, atol=1e-12)
+# C1 / C2 / C4 reference trajectories: tests/test_gpu_trajectories.py
 
 
 def test_partitioned_engine_single_rank(H):

@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-4)
     ap.add_argument("--workers", type=int, default=8)
     a = ap.parse_args()
-    doc, mon, lpa = scuc.build_config(a.config, device="cuda:0")
+    doc, mon, lpa = scuc.build_config(a.config)
     rng = np.random.default_rng(0)
     lps = []
     for _ in range(a.copies):

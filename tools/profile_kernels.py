@@ -26,7 +26,7 @@ from paper_2510_10891_b200.lp import Precision  # noqa: E402
 
 NAMES = {0: "spmv_A", 1: "spmv_AT", 2: "update_primal", 3: "update_dual",
          5: "spmv_AT+primal", 6: "spmv_A+dual"}
-doc, mon, lpa = scuc.build_config(a.config, device="cuda:0")
+doc, mon, lpa = scuc.build_config(a.config)
 eng = hprlp.Engine(lpa.to_lp(), reorder=bool(a.reorder))
 eng.solve_raw(hprlp.SolverConfig(tolerance=1e-4, ruiz=False, precision=Precision(a.precision),
                                  max_iterations=0))

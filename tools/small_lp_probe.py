@@ -15,7 +15,7 @@ for name, tri, tol in (("C1", None, 1e-4), ("C1", None, 1e-6), ("C2", 500, 1e-4)
         doc = scuc.generate_instance(**scuc.CONFIGS[name])
         lpa = scuc.build_relaxation(doc, scuc.all_base_triples(doc))
     else:
-        doc, mon, lpa = scuc.build_config(name, n_triples=tri, device="cuda:0")
+        doc, mon, lpa = scuc.build_config(name, n_triples=tri)
     lp = lpa.to_lp()
     torch.cuda.synchronize()
     t0 = time.perf_counter()

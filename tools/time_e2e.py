@@ -4,7 +4,7 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2510_10891_b200 import hprlp, scuc
-doc, mon, lpa = scuc.build_config("C4", device="cuda:0")
+doc, mon, lpa = scuc.build_config("C4")
 cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, max_iterations=200000)
 for rep in range(2):
     lp = lpa.to_lp()

@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2510_10891_b200 import hprlp, scuc
-t = time.perf_counter(); doc, mon, lpa = scuc.build_config("C4", device="cuda:0"); print("build", round(time.perf_counter() - t, 2))
+t = time.perf_counter(); doc, mon, lpa = scuc.build_config("C4"); print("build", round(time.perf_counter() - t, 2))
 for rep in range(2):
     lp = lpa.to_lp()
     t = time.perf_counter(); csc = lp.matrix.csc; tc = time.perf_counter() - t
