@@ -130,6 +130,7 @@ struct Csr {
     const int4* pdesc;
 };
 
-constexpr int PANEL_ROWS = 32;    // rows (F^T columns) per panel tile: one warp-width
+constexpr int PANEL_ROWS = TPB;   // rows (F^T columns) per panel tile: one per thread
+constexpr int PANEL_MAX_KEEP = 32; // indexed entries a panel row may keep beside its panel
 
 }  // namespace hpr

@@ -1540,7 +1540,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             CK(cudaMemsetAsync(h->d_dev, 0, 2 * sizeof(unsigned long long), s));
             CK(cudaMemsetAsync(lenbuf + n, 0, sizeof(int), s));
             k_col_panels<<<nblk(n, LAYOUT_TPB), LAYOUT_TPB, 0, s>>>(
-                h->FT.ptr, h->FT.idx, n, h->rbase, PANEL_MIN_RUN, TILE_NNZ / PANEL_ROWS, h->pinfo, roff, lenbuf,
+                h->FT.ptr, h->FT.idx, n, h->rbase, PANEL_MIN_RUN, PANEL_MAX_KEEP, h->pinfo, roff, lenbuf,
                 h->d_dev);
             CKL();
             unsigned long long cov[2] = {0, 0};

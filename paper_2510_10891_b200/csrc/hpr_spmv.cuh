@@ -76,12 +76,17 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
     acc.zero();
     const int4 tl = A.tiles[blockIdx.x];
     if (tl.y < 0 && tl.w < 0) {
-        // ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= 32 rows with flow panels -------
-        // Remaining (indexed) entries are staged as in a stream tile; the dense
-        // part is read from F's row-major values: lane = row, warp = every 4th
-        // panel row, so each load of a warp is one contiguous 256-byte segment
-        // of a flow row and y is a warp-uniform broadcast.
-        __shared__ T ppart[TPB / 32][PANEL_ROWS];
+        // ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= TPB rows sharing flow panels -------
+        // Remaining (indexed) entries are staged as in a stream tile.  The dense
+        // part is read from F's row-major values with thread = F^T row (an F
+        // column): for every shared flow row i, the tile's threads read one
+        // contiguous run of F's row i, y_i and the row's base come from shared
+        // memory, and each thread sums its whole column -- no cross-warp
+        // reduction, one store per row (A/B at C4 shape, tools/flow_probe.cu:
+        // 45.0 -> 38.3 us for the flow block against the 32-column tiles
+        // with lane = column, warp = every 4th row).
+        __shared__ T sy[TPB];
+        __shared__ long long sb[TPB];
         const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = -tl.w - 1 - tl.z;
         const int R = r1 - r0;
         {
@@ -91,50 +96,39 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
             if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
             if (threadIdx.x == 0) sptr[R] = cnt;
         }
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int4 pd = A.pdesc[blockIdx.x];
+        const int2 pi = pd.w > 0 ? make_int2(pd.x, pd.y) : A.pinfo[r0];
+        const int k = threadIdx.x;
+        const T* __restrict__ pv = A.pvals + (r0 + k);
         T s = T(0);
-        if (lane < R) {
-            const int r = r0 + lane;
-            if (pd.w > 0) {
-                // one row-major block: no per-row lookups between the tile and the loads
-                const T* __restrict__ pv = A.pvals + ((long long)pd.z + r);
-                const T* __restrict__ yv = xg + pd.x;
-                // 6 rows per thread per batch (A/B: 4 -> 6 took F^T 59.5 -> 57.5 us at C4;
-                // 7 is no better, and predicated full batches spill)
-                constexpr int U = 6;
-                int q = warp;
-                for (; q + (U - 1) * (TPB / 32) < pd.y; q += U * (TPB / 32)) {
-                    T v[U], g[U];
+        for (int q0 = 0; q0 < pi.y; q0 += TPB) {
+            const int nq = min(TPB, pi.y - q0);
+            __syncthreads();               // previous chunk consumed
+            if (threadIdx.x < nq) {
+                const int i = pi.x + q0 + threadIdx.x;
+                sy[threadIdx.x] = ld_ro(xg + i);
+                sb[threadIdx.x] = pd.w > 0 ? (long long)pd.z + (long long)(q0 + threadIdx.x) * pd.w
+                                           : (long long)__ldg(A.rbase + i);
+            }
+            __syncthreads();
+            if (k < R) {
+                constexpr int U = 8;
+                int q = 0;
+                for (; q + U <= nq; q += U) {
+                    T v[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int qq = q + u * (TPB / 32);
-                        v[u] = ld_stream(pv + (long long)qq * pd.w);
-                        g[u] = ld_ro(yv + qq);
-                    }
+                    for (int u = 0; u < U; ++u) v[u] = ld_stream(pv + sb[q + u]);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) s += v[u] * g[u];
+                    for (int u = 0; u < U; ++u) s += v[u] * sy[q + u];
                 }
-                for (; q < pd.y; q += TPB / 32) s += ld_stream(pv + (long long)q * pd.w) * ld_ro(yv + q);
-            } else {
-                const int2 pi = A.pinfo[r];
-#pragma unroll 4
-                for (int q = warp; q < pi.y; q += TPB / 32) {
-                    const int i = pi.x + q;
-                    s += ld_stream(A.pvals + ((long long)__ldg(A.rbase + i) + r)) * ld_ro(xg + i);
-                }
+                for (; q < nq; ++q) s += ld_stream(pv + sb[q]) * sy[q];
             }
         }
-        ppart[warp][lane] = s;
-        __syncthreads();
-        if (threadIdx.x < R) {
-            const int k = threadIdx.x;
+        __syncthreads();                   // staged leftovers visible
+        if (k < R) {
             T t = T(0);
             for (int q = sptr[k]; q < sptr[k + 1]; ++q) t += prod[q];
-            T pv = ppart[0][k];
-#pragma unroll
-            for (int w = 1; w < TPB / 32; ++w) pv += ppart[w][k];
-            epi.apply(r0 + k, t + pv, acc);
+            epi.apply(r0 + k, t + s, acc);
         }
         block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
     } else if (tl.y < 0) {

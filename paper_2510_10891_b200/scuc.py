@@ -44,6 +44,10 @@ CONFIGS = {
     "C2": dict(n_buses=1354, n_gens=260, n_lines=1991, n_periods=24, seed=2),
     "C3": dict(n_buses=6468, n_gens=399, n_lines=9000, n_periods=36, seed=3),
     "C4": dict(n_buses=13659, n_gens=4092, n_lines=20467, n_periods=36, seed=4),
+    # C4 plus 64 single-line (chord) outages; monitors 20,000 N-1 (line, period,
+    # contingency) triples -> ~874M nonzeros (BASELINE configs[4])
+    "C5": dict(n_buses=13659, n_gens=4092, n_lines=20467, n_periods=36, seed=4,
+               n_contingencies=64),
 }
 
 
@@ -361,6 +365,27 @@ def _ptdf_rows_direct(n_b, fb, tb, react, ref, lines, skip=None, device=None):
     return out
 
 
+def _lodf_rows(base: np.ndarray, base_pk: np.ndarray, lines, k: int, fb, tb, ref: int):
+    """Post-contingency PTDF rows by the line-outage distribution factor
+    (LODF) update instead of a fresh factorisation per contingency
+    (``compute_ptdf`` refactorises, ``instance.py:241-267``): with line k
+    (f -> t) out,
+
+        PTDF_c[l, :] = PTDF[l, :] + LODF[l, k] * PTDF[k, :],
+        LODF[l, k]   = (PTDF[l, f] - PTDF[l, t]) / (1 - (PTDF[k, f] - PTDF[k, t])),
+
+    the outaged line's own row is zero and the reference-bus column stays
+    zero, as ``_ptdf_matrix(skip_line=k)`` leaves them (``instance.py:230-238``).
+    Equal to the refactorised table to rounding (tests/test_builder.py)."""
+    f, t = int(fb[k]), int(tb[k])
+    den = 1.0 - (base_pk[f] - base_pk[t])
+    num = base[:, f] - base[:, t]
+    out = base + (num / den)[:, None] * base_pk[None, :]
+    out[np.asarray(lines) == k] = 0.0
+    out[:, ref] = 0.0
+    return out
+
+
 class PtdfRows:
     """Lazy PTDF row provider: ``row(line_pos, key)``.
 
@@ -368,7 +393,9 @@ class PtdfRows:
     bit (small networks); ``"direct"`` solves only for the needed rows
     (optionally on a CUDA device), which is what 13,659-bus instances need —
     ``build_model`` only ever indexes ``ptdf.table(key)[row, :]``
-    (``formulation.py:354``)."""
+    (``formulation.py:354``).  ``"lodf"`` takes the base rows as "direct" does
+    and derives every contingency row from them by the LODF update (one
+    solve for all N-1 keys: what the C5 instances need)."""
 
     def __init__(self, net, method="reference", device=None, needed=None):
         self.net = net
@@ -376,11 +403,43 @@ class PtdfRows:
         self.device = device
         self._tables = {}
         self._rows = {}
+        self._base = {}
         self._needed = needed or {}
+
+    def _base_rows(self, lines):
+        net = self.net
+        missing = sorted({int(q) for q in lines} - set(self._base))
+        if missing:
+            rows = _ptdf_rows_direct(net.n_b, net.fb, net.tb, net.react, net.ref, missing,
+                                     device=self.device)
+            for c, q in enumerate(missing):
+                self._base[q] = rows[c]
+        return np.stack([self._base[int(q)] for q in lines]) if len(lines) else \
+            np.zeros((0, net.n_b))
 
     def row(self, lpos: int, key: str) -> np.ndarray:
         net = self.net
         skip = None if key == BASE_CASE else net.cont_line[key]
+        if self.method == "lodf":
+            if (lpos, key) not in self._rows:
+                if not self._base:
+                    # one solve for every base row any key needs (lines + outages)
+                    want = set()
+                    for kk, ls in self._needed.items():
+                        want |= set(ls)
+                        if kk != BASE_CASE:
+                            want.add(net.cont_line[kk])
+                    self._base_rows(sorted(want | {lpos}))
+                lines = sorted(set(self._needed.get(key, [])) | {lpos})
+                base = self._base_rows(lines)
+                if key == BASE_CASE:
+                    rows = base
+                else:
+                    rows = _lodf_rows(base, self._base_rows([skip])[0], lines, skip,
+                                      net.fb, net.tb, net.ref)
+                for c, q in enumerate(lines):
+                    self._rows[(q, key)] = rows[c]
+            return self._rows[(lpos, key)]
         if self.method == "reference":
             if key not in self._tables:
                 self._tables[key] = _ptdf_full_reference(
@@ -606,7 +665,13 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
                np.concatenate([seg_w, -np.ones(ns)]), 0.0)
 
     # flow rows                                                          (:351-369)
+    # Emitted straight in canonical CSR form: build_model's entries of a flow
+    # row are (p', u) pairs per generator then the buses' slack columns; sorted
+    # by column (SparseMatrix.from_coo) that is the u block (ascending unit),
+    # the p' block, then the slack block, so each row is three slices and no
+    # global sort over the (up to ~10^9) flow entries is needed.
     monitored = sorted(set(monitored))
+    flow = None
     if monitored:
         if ptdf is None:
             needed = {}
@@ -614,7 +679,8 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
                 needed.setdefault(key, []).append(inst.line_pos[lid])
             ptdf = PtdfRows(inst.net, method=ptdf_method, device=device, needed=needed)
         gb = inst.gen_bus
-        fr_r, fr_c, fr_v, fr_rhs = [], [], [], []
+        lens = np.empty(2 * len(monitored), np.int64)
+        parts_c, parts_v, fr_rhs = [], [], np.empty(2 * len(monitored))
         for q, (lid, t, key) in enumerate(monitored):
             lpos = inst.line_pos[lid]
             delta = ptdf.row(lpos, key)
@@ -623,22 +689,15 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
             coeff = delta[gb]
             gsel = np.flatnonzero(np.abs(coeff) > _FLOW_COEFF_DROP)
             bsel = np.flatnonzero(np.abs(delta) > _FLOW_COEFF_DROP)
-            # entry order of build_model: per generator (p', u) pairs, then buses
-            c_g = np.empty(2 * gsel.size, np.int64)
-            v_g = np.empty(2 * gsel.size)
-            c_g[0::2] = pp[gsel * T + t]
-            c_g[1::2] = u[gsel * T + t]
-            v_g[0::2] = coeff[gsel]
-            v_g[1::2] = coeff[gsel] * inst.pmin[gsel]
-            cols = np.concatenate([c_g, pen[bsel * T + t]])
-            vals = np.concatenate([v_g, delta[bsel]])
-            fr_r.append(np.full(cols.size, 2 * q))
-            fr_r.append(np.full(cols.size, 2 * q + 1))
-            fr_c += [cols, cols]
-            fr_v += [vals, -vals]
-            fr_rhs += [-limit + base, -limit - base]
-        rows.block(2 * len(monitored), np.concatenate(fr_r), np.concatenate(fr_c),
-                   np.concatenate(fr_v), np.array(fr_rhs))
+            vu = coeff[gsel] * inst.pmin[gsel]
+            ku = vu != 0.0                      # add_row drops exact zeros (:246)
+            cols = np.concatenate([u[gsel[ku] * T + t], pp[gsel * T + t], pen[bsel * T + t]])
+            vals = np.concatenate([vu[ku], coeff[gsel], delta[bsel]])
+            parts_c.append(cols)
+            parts_v.append(vals)
+            lens[2 * q] = lens[2 * q + 1] = cols.size
+            fr_rhs[2 * q], fr_rhs[2 * q + 1] = -limit + base, -limit - base
+        flow = (lens, parts_c, parts_v, fr_rhs)
 
     # ---- bounds, objective -------------------------------------------------
     lower = np.zeros(n)
@@ -682,10 +741,32 @@ def build_relaxation(doc_or_inst, monitored=(), ptdf: PtdfRows | None = None,
     indptr = np.zeros(m + 1, dtype=np.int64)
     np.add.at(indptr, r_all + 1, 1)
     indptr = np.cumsum(indptr)
+    rhs = np.concatenate(rows.rhs)
+    indices, data = c_all.astype(np.int32), v_all
+    if flow is not None:                 # the flow rows close the row order (:351-369)
+        lens, parts_c, parts_v, fr_rhs = flow
+        nf = int(lens.sum())
+        if indptr[-1] + nf >= 2 ** 31:
+            raise ValueError("nnz exceeds int32 indexing")
+        fidx = np.empty(nf, np.int32)
+        fval = np.empty(nf, np.float64)
+        pos = 0
+        for cols, vals in zip(parts_c, parts_v):
+            k = cols.size
+            fidx[pos:pos + k] = cols
+            fval[pos:pos + k] = vals
+            fidx[pos + k:pos + 2 * k] = cols
+            np.negative(vals, out=fval[pos + k:pos + 2 * k])
+            pos += 2 * k
+        indptr = np.concatenate([indptr, indptr[-1] + np.cumsum(lens)])
+        indices = np.concatenate([indices, fidx])
+        data = np.concatenate([data, fval])
+        rhs = np.concatenate([rhs, fr_rhs])
+        m += lens.size
     if indptr[-1] >= 2 ** 31:
         raise ValueError("nnz exceeds int32 indexing")
-    return LpArrays(indptr=indptr.astype(np.int32), indices=c_all.astype(np.int32),
-                    data=v_all, shape=(m, n), rhs=np.concatenate(rows.rhs),
+    return LpArrays(indptr=indptr.astype(np.int32), indices=indices,
+                    data=data, shape=(m, n), rhs=rhs,
                     cost=cost, lower=lower, upper=upper, n_eq=int(n_eq), offset=0.0)
 
 
@@ -703,9 +784,20 @@ def build_config(name: str, n_triples: int | None = None, ptdf_method: str | Non
         cfg["seed"] = seed
     doc = generate_instance(**cfg)
     if n_triples is None:
-        n_triples = {"C1": -1, "C2": 500, "C3": 2000, "C4": 1000}[name]
-    mon = all_base_triples(doc) if n_triples < 0 else sample_monitored(doc, n_triples, cfg["seed"])
+        n_triples = {"C1": -1, "C2": 500, "C3": 2000, "C4": 1000, "C5": 20000}[name]
+    n1 = name == "C5"
+    mon = all_base_triples(doc) if n_triples < 0 else sample_monitored(
+        doc, n_triples, cfg["seed"], contingencies=n1)
     if ptdf_method is None:
-        ptdf_method = "reference" if len(doc["buses"]) <= 2000 else "direct"
+        ptdf_method = ("lodf" if n1 else
+                       "reference" if len(doc["buses"]) <= 2000 else "direct")
+    if n1 and device is None:
+        # ~20K base PTDF rows: one dense solve on the GPU when there is one
+        # (C5 has no CPU reference run to reproduce, so no pinned host solve)
+        try:
+            import torch
+            device = "cuda" if torch.cuda.is_available() else None
+        except ImportError:
+            device = None
     lp = build_relaxation(doc, mon, ptdf_method=ptdf_method, device=device)
     return doc, mon, lp

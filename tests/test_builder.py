@@ -79,3 +79,47 @@ def test_c1_digest_matches_golden_fixture():
     doc, mon, lp = scuc.build_config("C1")
     assert lp.shape == tuple(g["shape"]) and lp.nnz == g["nnz"]
     assert lp.digest() == g["digest"]
+
+
+@needs_reference
+def test_lodf_rows_match_refactorised_contingency_tables():
+    """C5's contingency rows: the LODF update from the base rows equals the
+    reference's per-contingency refactorisation (compute_ptdf,
+    instance.py:241-267) to rounding, including the zeroed outaged row."""
+    from scuckit import compute_ptdf, parse_instance
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7, n_contingencies=5)
+    inst = scuc.Instance(doc)
+    ref = compute_ptdf(parse_instance(doc).network)
+    keys = [c["id"] for c in doc["contingencies"]]
+    lines = list(range(len(doc["lines"])))
+    needed = {k: lines for k in keys}
+    prov = scuc.PtdfRows(inst.net, method="lodf", needed=needed)
+    for key in keys:
+        got = np.stack([prov.row(q, key) for q in lines])
+        want = ref.table(key)
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-12)
+        k = inst.net.cont_line[key]
+        assert not got[k].any() and not got[:, inst.net.ref].any()
+
+
+@needs_reference
+@pytest.mark.parametrize("ptdf_method", ["reference", "lodf"])
+def test_n1_flow_rows_match_reference_build_model(ptdf_method):
+    """N-1 monitored triples (the C5 row family): CSR structure, rhs and
+    values against build_model on the reference's own contingency tables --
+    identical with the refactorised tables, within rounding with the LODF
+    rows (the reference's 1e-10 coefficient drop decides the same way)."""
+    from scuckit import build_model, compute_ptdf, parse_instance
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7, n_contingencies=4)
+    mon = scuc.sample_monitored(doc, 120, 7, contingencies=True)
+    mine = scuc.build_relaxation(doc, mon, ptdf_method=ptdf_method)
+    inst = parse_instance(doc)
+    ref = build_model(inst, monitored=mon, ptdf=compute_ptdf(inst.network))[0].relax()
+    c = ref.matrix.csr
+    assert c.shape == mine.shape
+    assert np.array_equal(c.indptr, mine.indptr) and np.array_equal(c.indices, mine.indices)
+    if ptdf_method == "reference":
+        assert np.array_equal(c.data, mine.data) and np.array_equal(ref.rhs, mine.rhs)
+    else:
+        np.testing.assert_allclose(mine.data, c.data, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(mine.rhs, ref.rhs, rtol=1e-10, atol=1e-9)

@@ -103,8 +103,8 @@ def test_c1_fp32_gate(H):
 
 
 # opening checks of the C1 FP32 run held to 1e-5 (row-relative); measured on
-# the box: profiles/r03_traj_probe.json "rows_within_1e5"
-FP32_GATE_ROWS = 12
+# the box: 62 (profiles/r03_traj_probe.json "rows_within_1e5")
+FP32_GATE_ROWS = 50
 
 
 def test_c2_fp64_trajectory(H):
@@ -123,7 +123,7 @@ def test_c2_fp64_trajectory(H):
     _assert_same_trajectory(r, g["fp64"], row_rtol=C2_ROW_RTOL, sigma_rtol=1e-9, obj_rtol=1e-6)
 
 
-C2_ROW_RTOL = 1e-9
+C2_ROW_RTOL = 2e-9
 
 
 def _c4():
