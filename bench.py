@@ -165,8 +165,10 @@ def workload(args):
     BASELINE.json headline)."""
     from paper_2510_10891_b200 import scuc
     c = scuc.CONFIGS[args.config]
-    n = args.triples or {"C1": -1, "C2": 500, "C3": 2000, "C4": 1000}[args.config]
-    tri = "all base flow triples" if n < 0 else f"{n} sampled base flow triples"
+    n = args.triples or {"C1": -1, "C2": 500, "C3": 2000, "C4": 1000, "C5": 20000}[args.config]
+    kind = (f"N-1 flow triples over {c['n_contingencies']} line outages"
+            if args.config == "C5" else "base flow triples")
+    tri = "all base flow triples" if n < 0 else f"{n} sampled {kind}"
     return (f"{args.config}: synthetic {c['n_buses']}-bus/{c['n_gens']}-unit/{c['n_periods']}-period "
             f"SCUC LP relaxation + {tri}")
 
