@@ -663,7 +663,13 @@ _PRESOLVE_SITES = ("scuckit.presolve", "scuckit.fixing", "scuckit.milp_bb", "scu
 _SCREEN_SITES = ("scuckit.driver", "scuckit")
 
 
-def install(module=None, presolve: bool = True, screen: bool = True):
+# where the reference imported the model builder / PTDF by name
+_BUILDER_SITES = {"build_model": ("scuckit.formulation", "scuckit.driver", "scuckit"),
+                  "compute_ptdf": ("scuckit.instance", "scuckit.formulation", "scuckit.driver",
+                                   "scuckit")}
+
+
+def install(module=None, presolve: bool = True, screen: bool = True, builder: bool = True):
     """Route the reference's LP solves to the GPU engine.
 
     Rebinds ``scuckit.hprlp.solve`` (and ``kkt_residual`` / ``hpr_iterate``)
@@ -674,7 +680,12 @@ def install(module=None, presolve: bool = True, screen: bool = True):
     mirror in ``paper_2510_10891_b200.presolve`` (bit-identical reductions).
     With ``screen`` the driver's post-MILP flow screen
     (``driver.screen_violations``, ``driver.py:165-200``, called by name at
-    ``:288``) is rebound to the device screen in ``screen.py``."""
+    ``:288``) is rebound to the device screen in ``screen.py``.  With
+    ``builder`` the model construction the driver runs every filtering pass
+    (``build_model``, ``driver.py:249-250``; ``compute_ptdf``, ``:210``) is
+    rebound to ``builder.py``: the reference's own model objects, built
+    vectorised (identical rows, bounds and tags), PTDF tables from one solve
+    plus LODF updates."""
     import importlib
     if module is None:
         import scuckit.hprlp as module
@@ -708,6 +719,14 @@ def install(module=None, presolve: bool = True, screen: bool = True):
             if hasattr(mod, "screen_violations"):
                 _SAVED.setdefault("screen", {}).setdefault(name, mod.screen_violations)
                 mod.screen_violations = dev_screen.screen_violations
+    if builder:
+        from . import builder as fast
+        for fn, sites in _BUILDER_SITES.items():
+            for name in sites:
+                mod = importlib.import_module(name)
+                if hasattr(mod, fn):
+                    _SAVED.setdefault("builder", {}).setdefault((name, fn), getattr(mod, fn))
+                    setattr(mod, fn, getattr(fast, fn))
     return module
 
 
@@ -723,6 +742,8 @@ def uninstall():
         setattr(importlib.import_module(name), fn, orig)
     for name, orig in _SAVED.get("screen", {}).items():
         importlib.import_module(name).screen_violations = orig
+    for (name, fn), orig in _SAVED.get("builder", {}).items():
+        setattr(importlib.import_module(name), fn, orig)
     from . import presolve as native
     native._LOG_CLASS = native.ReductionLog
     from . import screen as dev_screen

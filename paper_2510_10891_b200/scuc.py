@@ -250,6 +250,12 @@ class LpArrays:
         h.update(f"{self.shape}{self.n_eq}{self.offset!r}".encode())
         return h.hexdigest()
 
+    def digest_parts(self) -> dict:
+        """Per-array digests (which part of two LPs differs)."""
+        import hashlib
+        return {k: hashlib.sha256(np.ascontiguousarray(getattr(self, k)).tobytes()).hexdigest()[:16]
+                for k in ("indptr", "indices", "data", "rhs", "cost", "lower", "upper")}
+
     def to_lp(self):
         """As a duck-typed StandardFormLp (``.matrix.csr/.csc``, vectors)."""
         from .lp import StandardFormLp, SparseMatrix
@@ -511,6 +517,50 @@ class Instance:
         self.seg_caps = [[float(s["p_max"]) for s in g["segments"]] for g in gens]
         self.seg_costs = [[float(s["cost"]) for s in g["segments"]] for g in gens]
         self.H = np.array([len(c) for c in self.seg_caps], dtype=np.int64)
+
+    @classmethod
+    def from_scuckit(cls, inst) -> "Instance":
+        """The same array view of a parsed (and possibly instance-scaled)
+        reference ``ScucInstance`` (``instance.py:29-139``,
+        ``formulation.apply_instance_scaling`` :148-191): what the drop-in
+        ``build_model`` reads, so scaled MW / $ values reach the rows exactly
+        as the reference's generator and bus attributes carry them."""
+        self = cls.__new__(cls)
+        self.doc = None
+        net = inst.network
+        self.T = int(inst.n_periods)
+        self.penalty = float(inst.penalty_cost)
+        self.bus_ids = [b.bid for b in net.buses]
+        bidx = net.bus_index()
+        self.B = len(net.buses)
+        self.demand = inst.demand_matrix()
+        lines = net.lines
+        self.line_ids = [ln.lid for ln in lines]
+        self.line_pos = net.line_index()
+        fb = np.array([bidx[ln.from_bus] for ln in lines], dtype=np.int64)
+        tb = np.array([bidx[ln.to_bus] for ln in lines], dtype=np.int64)
+        react = np.array([ln.reactance for ln in lines], dtype=np.float64)
+        self.limit = np.array([ln.limit for ln in lines], dtype=np.float64)
+        self.elimit = np.array([ln.emergency_limit for ln in lines], dtype=np.float64)
+        cont_line = {c.cid: self.line_pos[c.line] for c in net.contingencies}
+        self.net = _Net(self.B, fb, tb, react, bidx[net.reference_bus], cont_line)
+        gens = inst.generators
+        self.G = len(gens)
+        self.gen_bus = np.array([bidx[g.bus] for g in gens], dtype=np.int64)
+        f = lambda k: np.array([float(getattr(g, k)) for g in gens], dtype=np.float64)  # noqa: E731
+        self.pmin, self.pmax = f("p_min"), f("p_max")
+        self.min_cost = f("min_output_cost")
+        self.ru, self.rd = f("ramp_up"), f("ramp_down")
+        self.su, self.sd = f("startup_limit"), f("shutdown_limit")
+        self.init_power = f("initial_power")
+        self.init_on = np.array([int(g.initial_on) for g in gens], dtype=np.int64)
+        self.init_per = np.array([int(g.initial_periods) for g in gens], dtype=np.int64)
+        self.min_up = np.array([int(g.min_up) for g in gens], dtype=np.int64)
+        self.min_down = np.array([int(g.min_down) for g in gens], dtype=np.int64)
+        self.seg_caps = [[float(c) for c in g.segment_caps] for g in gens]
+        self.seg_costs = [[float(c) for c in g.segment_costs] for g in gens]
+        self.H = np.array([len(c) for c in self.seg_caps], dtype=np.int64)
+        return self
 
     def widths(self, g):
         prev = float(self.pmin[g])

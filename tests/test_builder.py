@@ -123,3 +123,87 @@ def test_n1_flow_rows_match_reference_build_model(ptdf_method):
     else:
         np.testing.assert_allclose(mine.data, c.data, rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(mine.rhs, ref.rhs, rtol=1e-10, atol=1e-9)
+
+
+def _same_model(a, b):
+    la, lb = a[0].lp, b[0].lp
+    ca, cb = la.matrix.csr, lb.matrix.csr
+    assert ca.shape == cb.shape and la.n_eq == lb.n_eq
+    assert np.array_equal(ca.indptr, cb.indptr) and np.array_equal(ca.indices, cb.indices)
+    assert np.array_equal(ca.data, cb.data)
+    for f in ("rhs", "cost", "lower", "upper"):
+        assert np.array_equal(getattr(la, f), getattr(lb, f)), f
+    assert la.row_tags == lb.row_tags and la.col_tags == lb.col_tags
+    assert np.array_equal(a[0].integrality, b[0].integrality)
+    assert a[1].n_cols == b[1].n_cols and np.array_equal(a[1].pprime, b[1].pprime)
+
+
+@needs_reference
+@pytest.mark.parametrize("args", [(30, 12, 45, 8, 3, -1, 0), (60, 20, 90, 12, 7, 40, 0),
+                                  (118, 54, 186, 24, 1, 300, 0), (60, 20, 90, 12, 7, 80, 3)])
+def test_dropin_build_model_identical_to_reference(args):
+    """builder.build_model (the install()ed replacement) against the
+    reference's build_model on the instance-scaled instance the driver uses
+    (driver.py:211-212, :249-250): CSR, rhs, bounds, costs, row and column
+    tags, integrality -- identical, with base and N-1 triples."""
+    from scuckit import apply_instance_scaling, build_model, compute_ptdf, parse_instance
+    from paper_2510_10891_b200 import builder
+    B, G, L, T, seed, ntr, nc = args
+    doc = scuc.generate_instance(B, G, L, T, seed=seed, n_contingencies=nc)
+    inst = parse_instance(doc)
+    ptdf = compute_ptdf(inst.network)
+    work, _ = apply_instance_scaling(inst)
+    mon = (scuc.all_base_triples(doc) if ntr < 0 else
+           scuc.sample_monitored(doc, ntr, seed, contingencies=nc > 0))
+    _same_model(builder.build_model(work, mon, ptdf), build_model(work, monitored=mon, ptdf=ptdf))
+    _same_model(builder.build_model(work, (), ptdf), build_model(work, monitored=(), ptdf=ptdf))
+
+
+@needs_reference
+def test_dropin_build_model_errors_like_reference():
+    from scuckit import build_model, parse_instance
+    from scuckit.formulation import ModelError
+    from paper_2510_10891_b200 import builder
+    doc = scuc.generate_instance(12, 6, 18, 6, seed=5)
+    inst = parse_instance(doc)
+    for bad in [("l999", 0, "base"), ("l0", 6, "base"), ("l0", 0, "c9")]:
+        with pytest.raises(ModelError) as mine:
+            builder.build_model(inst, [bad])
+        with pytest.raises(ModelError) as ref:
+            build_model(inst, monitored=[bad])
+        assert str(mine.value) == str(ref.value)
+
+
+@needs_reference
+def test_dropin_compute_ptdf_matches_reference():
+    from scuckit import compute_ptdf, parse_instance
+    from paper_2510_10891_b200 import builder
+    doc = scuc.generate_instance(60, 20, 90, 12, seed=7, n_contingencies=4)
+    net = parse_instance(doc).network
+    a, b = builder.compute_ptdf(net, device=None), compute_ptdf(net)
+    assert type(a) is type(b) and a.keys() == b.keys()
+    assert a.line_ids == b.line_ids and a.bus_ids == b.bus_ids
+    for k in b.keys():
+        np.testing.assert_allclose(a.table(k), b.table(k), rtol=0, atol=1e-12)
+
+
+@needs_reference
+def test_install_rebinds_builder_everywhere():
+    """install() routes the driver's per-pass model construction to the
+    vectorised builder (driver.py:210, :249-250) and uninstall() restores it."""
+    import scuckit
+    import scuckit.driver
+    import scuckit.formulation
+    import scuckit.instance
+    from paper_2510_10891_b200 import builder, hprlp
+    orig = scuckit.driver.build_model, scuckit.driver.compute_ptdf
+    hprlp.install()
+    try:
+        for mod in (scuckit, scuckit.driver, scuckit.formulation):
+            assert mod.build_model is builder.build_model
+        for mod in (scuckit, scuckit.driver, scuckit.formulation, scuckit.instance):
+            assert mod.compute_ptdf is builder.compute_ptdf
+    finally:
+        hprlp.uninstall()
+    assert (scuckit.driver.build_model, scuckit.driver.compute_ptdf) == orig
+    assert scuckit.formulation.build_model is not builder.build_model

@@ -121,3 +121,48 @@ def test_successive_fixing_c1_against_reference_record():
         assert abs(og - r["objective"]) <= 1e-6 * abs(r["objective"])
     want = {int(k): v for k, v in g["fixed"].items()}
     _assert_fixed_sets(rec, 0.1, (fixed, err), (want, g["error"]), "C1 vs reference record")
+
+
+def _report(rep):
+    d = rep.to_json_dict()
+    d.pop("timings")
+    return d
+
+
+def _assert_same_run(got, want, what):
+    assert got["status"] == want["status"] == "solved", what
+    assert got["exit_code"] == want["exit_code"]
+    assert abs(got["objective"] - want["objective"]) <= 1e-9 * abs(want["objective"]), what
+    assert got["monitored"] == want["monitored"]
+    assert got.get("commitment") == want.get("commitment")
+    assert got["fixing"] == want["fixing"]
+    assert got["nodes_total"] == want["nodes_total"]
+    assert len(got["passes"]) == len(want["passes"])
+    for a, b in zip(got["passes"], want["passes"]):
+        for k in ("stage", "index", "monitored_rows", "free_binaries", "milp_status",
+                  "milp_nodes", "violations_found"):
+            assert a[k] == b[k], (what, k, a[k], b[k])
+        assert abs(a["milp_gap"] - b["milp_gap"]) <= 1e-5
+
+
+def test_driver_run_completes_like_reference():
+    """North-star end-to-end criterion: the reference's own two-stage driver
+    (driver.run, driver.py:203-324) run to completion on a small instance,
+    once on its CPU path and once with install() routing LP solves, presolve,
+    the flow screen and the model builder to this package.  Same final MILP
+    objective (HiGHS-polished incumbent, milp_bb.py:146-162), commitment,
+    monitored set, fixing record per round, B&B nodes and pass records -- also
+    against the reference's record from the build container
+    (tests/golden/sf_small.json, make_sf_golden.py)."""
+    from scuckit import driver, parse_instance
+    from paper_2510_10891_b200 import hprlp as gpu, scuc
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "sf_small.json")))
+    doc = scuc.generate_instance(**g["instance"])
+    cpu = _report(driver.run(parse_instance(doc), driver.DriverConfig(time_limit=600.0)))
+    gpu.install()
+    try:
+        got = _report(driver.run(parse_instance(doc), driver.DriverConfig(time_limit=600.0)))
+    finally:
+        gpu.uninstall()
+    _assert_same_run(cpu, g["report"], "reference on the box vs its record")
+    _assert_same_run(got, cpu, "B200 path vs reference on the box")
