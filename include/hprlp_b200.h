@@ -222,7 +222,7 @@ typedef struct hpr_layout {
     int64_t ft_nnz;            /* entries left in F^T */
     int64_t index_free_nnz_f;  /* entries of F streamed without their column index */
     int32_t fused;             /* 1: the row-wise updates run as the products' epilogues */
-    int32_t reserved;
+    int32_t row_panel_groups;  /* dense F row groups read as row panels by A x~ (x~ once per slab) */
 } hpr_layout;
 int hpr_get_layout(hpr_handle* h, hpr_layout* out);
 

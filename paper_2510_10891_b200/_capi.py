@@ -95,7 +95,7 @@ class Layout(C.Structure):
                 ("tiles_ft", C.c_int32), ("reordered", C.c_int32), ("folded", C.c_int32),
                 ("workspace_bytes", C.c_size_t), ("panel_cols", C.c_int64),
                 ("panel_nnz", C.c_int64), ("f_nnz", C.c_int64), ("ft_nnz", C.c_int64),
-                ("index_free_nnz_f", C.c_int64), ("fused", C.c_int32), ("reserved", C.c_int32)]
+                ("index_free_nnz_f", C.c_int64), ("fused", C.c_int32), ("row_panel_groups", C.c_int32)]
 
 
 class ScreenInfo(C.Structure):

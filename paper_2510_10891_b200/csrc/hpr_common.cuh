@@ -90,6 +90,10 @@ struct Ctrl {
     // the function Python's float ** calls -- and relaunches the loop
     int sigma_pending;
     double sigma_ratio;
+    // queued blocks (partitioned loop): once a check stops the loop or needs
+    // the host's sigma update, `halt` turns every later loop kernel into a
+    // no-op until the host clears it; `skipped` marks a check that did not run
+    int halt, skipped;
     long long checks;
     // logging
     long long n_log, log_cap;
@@ -128,7 +132,22 @@ struct Csr {
     // i0 .. i0+L-1 and those F rows form one row-major block, so
     // F(i0+q, r) = pvals[base + q*stride + r] (stride 0: use pinfo / rbase)
     const int4* pdesc;
+    // loop launches only: Ctrl::halt (the product is skipped while it is set)
+    const int* halt;
+    // row panels (F only): groups of <= RP_ROWS consecutive dense rows over
+    // the same column run {r0, R, c0, len}; tile {-(g+1), column tile, 0, 0}
+    // sums a RP_COLS-column slab of every row of group g with x~ read once;
+    // the group's last tile (ticket gcount[g]) adds the slab partials
+    // gpart[gslot[g] + r * ntiles_g + t] in slab order
+    const int4* gdesc;
+    const int* gslot;
+    int* gcount;
+    double* gpart;
 };
+
+constexpr int RP_ROWS = 32;       // rows per row-panel group
+constexpr int RP_MIN_ROWS = 8;    // fewer dense rows sharing a run: chunk tiles instead
+constexpr int RP_COLS = 128;      // columns per row-panel tile (4 per lane)
 
 constexpr int PANEL_ROWS = TPB;   // rows (F^T columns) per panel tile: one per thread
 constexpr int PANEL_MAX_KEEP = 32; // indexed entries a panel row may keep beside its panel

@@ -151,16 +151,41 @@ inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 struct Plan {
     std::vector<int4> tiles, longs;
+    std::vector<int4> groups;     // row panels {r0, R, c0, len}
+    std::vector<int> gslot;       // first partial slot per group
+    long long nslots = 0;         // row-panel partial slots
 };
 
-// Cut a CSR into stream tiles and long-row chunks (see hpr_spmv.cuh).
-Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr) {
+// Cut a CSR into stream tiles and long-row chunks (see hpr_spmv.cuh).  With
+// `rb` (F's per-row base, INT_MIN unless the row is one consecutive-column
+// run), runs of >= RP_MIN_ROWS long dense rows over the same column run
+// become row-panel groups instead of per-row chunks.
+Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr,
+                 const int32_t* rb = nullptr) {
     Plan p;
     int r = 0;
     auto panel = [&](int q) { return pinfo && pinfo[q].y > 0; };
     auto same = [&](int a, int b) { return pinfo[a].x == pinfo[b].x && pinfo[a].y == pinfo[b].y; };
+    auto dense_long = [&](int q) {
+        return rb && rb[q] != INT_MIN && ptr[q + 1] - ptr[q] > TILE_NNZ;
+    };
+    auto run_of = [&](int q) { return std::make_pair(ptr[q] - rb[q], ptr[q + 1] - ptr[q]); };
     while (r < rows) {
         const int len = ptr[r + 1] - ptr[r];
+        if (dense_long(r)) {
+            int r1 = r + 1;
+            while (r1 < rows && r1 - r < RP_ROWS && dense_long(r1) && run_of(r1) == run_of(r)) ++r1;
+            if (r1 - r >= RP_MIN_ROWS) {
+                const int g = (int)p.groups.size();
+                const int c0 = ptr[r] - rb[r], nct = (len + RP_COLS - 1) / RP_COLS;
+                p.groups.push_back(make_int4(r, r1 - r, c0, len));
+                p.gslot.push_back((int)p.nslots);
+                p.nslots += (long long)(r1 - r) * nct;
+                for (int ct = 0; ct < nct; ++ct) p.tiles.push_back(make_int4(-(g + 1), ct, 0, 0));
+                r = r1;
+                continue;
+            }
+        }
         if (panel(r)) {
             // panel tile: consecutive panel rows, remaining entries staged like a stream tile
             const int r0 = r;
@@ -246,6 +271,12 @@ struct DevCsr {
     long long free_nnz = 0;      // entries in index-free chunks
     int* counters = nullptr;
     double* tpart = nullptr;
+    int4* gdesc = nullptr;       // row panels (F only; hpr_common.cuh Csr::gdesc)
+    int* gslot = nullptr;
+    int* gcount = nullptr;
+    double* gpart = nullptr;
+    int ngroups = 0;
+    long long group_nnz = 0;
     template <typename T>
     Csr<T> view(const T* vals, const T* pvals = nullptr) const {
         Csr<T> c;
@@ -260,11 +291,16 @@ struct DevCsr {
         c.nlong = nlong;
         c.counters = counters;
         c.tile_part = tpart;
+        c.halt = nullptr;
         c.taux = taux;
         c.pvals = pvals;
         c.pinfo = pinfo;
         c.rbase = rbase;
         c.pdesc = pdesc;
+        c.gdesc = gdesc;
+        c.gslot = gslot;
+        c.gcount = gcount;
+        c.gpart = gpart;
         return c;
     }
     int nslots() const { return ntiles + nlong; }
@@ -348,6 +384,14 @@ size_t carve(hpr_handle* h, char* base) {
         M.tpart = cv.take<double>(tb.tiles);
         M.taux = cv.take<int2>(tb.tiles);
         M.pdesc = &M == &h->FT ? cv.take<int4>(tb.tiles) : nullptr;
+        if (&M == &h->F) {
+            // row panels: groups of >= RP_MIN_ROWS long rows, so at most one per
+            // RP_MIN_ROWS long rows; one partial per row per RP_COLS columns
+            M.gdesc = cv.take<int4>(tb.longs);
+            M.gslot = cv.take<int>(tb.longs);
+            M.gcount = cv.take<int>(tb.longs);
+            M.gpart = cv.take<double>(nnz / RP_COLS + tb.longs + 1);
+        }
     };
     csr(h->A, m, bm, false, false);
     csr(h->AT, n, bn, false, false);
@@ -579,9 +623,11 @@ double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only,
 
 template <typename T, class Epi>
 void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, const Epi& epi,
-                 cudaStream_t s, const T* pvals = nullptr) {
+                 cudaStream_t s, const T* pvals = nullptr, const int* halt = nullptr) {
     if (M.pinfo && !pvals) fail(HPR_ERR_INVALID, "internal: panel operand without F values");
-    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, M.view<T>(vals, pvals), xg, epi);
+    Csr<T> v = M.view<T>(vals, pvals);
+    v.halt = halt;
+    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, v, xg, epi);
     h->launches += 1;
 }
 
@@ -758,20 +804,31 @@ template <typename T>
 void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     double* pd = (double*)h->P;
     EpiStore<double> st{pd, nullptr};
-    launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s);
+    const int* halt = mode == 1 ? &h->ctrl->halt : nullptr;
+    launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s,
+                (const double*)nullptr, halt);
     // partitioned: every rank uses the same slot count so the row-side sums reduce slot-wise
     const int gr = h->comm ? ROW_GRID_MAX : row_grid(h->nf), gc = row_grid(h->n);
     CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     launch(k_check_rows<T>, gr, TPB, s, ar);
     allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
     launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s,
-                (const double*)h->F.mval);
+                (const double*)h->F.mval, halt);
     allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
     CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                         h->colpart};
     launch(k_check_cols<T>, gc, TPB, s, ac);
+    const int* tflag = nullptr;
+    if (h->comm && mode == 1) {
+        // partitioned: every rank's deadline verdict, MAX-reduced on the device,
+        // so the controllers (replicated, identical inputs) stop together
+        launch(k_deadline_flag, 1, 1, s, (const Ctrl*)h->ctrl, h->d_flag);
+        allreduce(h, h->d_flag, 1, ncclInt32, ncclMax, s);
+        tflag = h->d_flag;
+        h->launches += 1;
+    }
     launch(k_controller, 1, CTRL_TPB, s, h->ctrl, (const double*)h->rowpart, gr,
-           (const double*)h->colpart, gc, h->log, mode);
+           (const double*)h->colpart, gc, h->log, mode, tflag);
     const int len = std::max(h->n, h->m);
     launch(k_restart_copy<T>, row_grid(len), TPB, s, (const Ctrl*)h->ctrl, h->n, h->m, h->nf,
            (const double*)h->XM, (const double*)h->YM, (const double*)h->ZM, h->BXm, h->BYm,
@@ -787,19 +844,21 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
         PrimalArgs<T> pa{h->ctrl, j, h->n, nullptr, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo,
                          p.up, p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
         launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, EpiPrimal<T, CHECK>{pa, nullptr}, s,
-                    p.f_vals);
+                    p.f_vals, &h->ctrl->halt);
         DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, nullptr, p.Y, p.AY, p.rhs, p.YF,
                        p.BY, p.BYF, h->YM, h->YMF, h->rs, h->frow};
-        launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, CHECK>{da, nullptr}, s);
+        launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, CHECK>{da, nullptr}, s,
+                    (const T*)nullptr, &h->ctrl->halt);
         return;
     }
     EpiStore<T> st{p.P, nullptr};
-    launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals);             // A^T y
+    const int* halt = &h->ctrl->halt;
+    launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals, halt);       // A^T y
     allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
     launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
-    launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s);                         // A x~
+    launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s, (const T*)nullptr, halt);  // A x~
     DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                    p.BY, p.BYF, h->YM, h->YMF, h->rs};
     launch(k_update_dual<T, CHECK>, nblk(h->m), TPB, s, da);
@@ -870,30 +929,24 @@ void ensure_graph(hpr_handle* h, const Ptrs<T>& p, int B) {
 // no rank leaves the collective sequence alone.
 bool host_sigma_update(hpr_handle* h);
 
-double run_loop_partitioned(hpr_handle* h, double time_left) {
+// Partitioned mode (and HPR_PLAIN): the block body as a plain graph, queued
+// PART_QUEUE blocks at a time with one host read of the controller per
+// queue.  A check that stops the loop (tolerance, limits, or the device-side
+// deadline flag MAX-reduced over the ranks) or that needs the host's sigma
+// update sets Ctrl::halt, which turns the rest of the queue into no-ops; every
+// rank runs the same collectives in the same order, so none is left waiting.
+constexpr int PART_QUEUE = 8;
+
+double run_loop_partitioned(hpr_handle* h, double /*time_left*/) {
     cudaStream_t s = h->stream;
-    const auto t0 = std::chrono::steady_clock::now();
     const long long t_before = h->h_ctrl->total;
     CK(cudaEventRecord(h->ev[2], s));
     while (true) {
-        CK(cudaGraphLaunch(h->gexec, s));
-        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        const int over = (time_left >= 0 && el > time_left) ? 1 : 0;
-        CK(cudaMemcpyAsync(h->d_flag, &over, sizeof(int), cudaMemcpyHostToDevice, s));
-        allreduce(h, h->d_flag, 1, ncclInt32, ncclMax, s);
-        int flag = 0;
+        for (int q = 0; q < PART_QUEUE; ++q) CK(cudaGraphLaunch(h->gexec, s));
         CK(cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(&h->h_scal[0], h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        std::memcpy(&flag, &h->h_scal[0], sizeof(int));
         if (h->h_ctrl->status != -1) break;
         host_sigma_update(h);            // replicated controller: same ratio on every rank
-        if (flag) {
-            h->h_ctrl->status = HPR_TIME_LIMIT;
-            CK(cudaMemcpyAsync(&h->ctrl->status, &h->h_ctrl->status, sizeof(int),
-                               cudaMemcpyHostToDevice, s));
-            break;
-        }
     }
     CK(cudaEventRecord(h->ev[3], s));
     CK(cudaStreamSynchronize(s));
@@ -916,10 +969,12 @@ bool host_sigma_update(hpr_handle* h) {
     if (!(f <= 4.0) && f == f) f = 4.0;
     c.sigma = c.sigma * f;
     c.sigma_pending = 0;
+    c.halt = 0;
     cudaStream_t s = h->stream;
     CK(cudaMemcpyAsync(&h->ctrl->sigma, &c.sigma, sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(&h->ctrl->sigma_pending, &c.sigma_pending, sizeof(int),
                        cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&h->ctrl->halt, &c.halt, sizeof(int), cudaMemcpyHostToDevice, s));
     return true;
 }
 
@@ -1101,13 +1156,13 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
         if (prm->time_limit >= 0) {
             const double rem = std::max(0.0, prm->time_limit - elapsed);
             time_left = rem;
-            if (!h->comm) {   // partitioned: agreed on the host per block
-                k_set_deadline<<<1, 1, 0, s>>>(h->ctrl, (unsigned long long)(rem * 1e9));
-                CKL();
-                h->launches++;
-                int one = 1;
-                CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
-            }
+            // every rank sets its own deadline; partitioned, the flags are
+            // MAX-reduced on the device before each controller (k_deadline_flag)
+            k_set_deadline<<<1, 1, 0, s>>>(h->ctrl, (unsigned long long)(rem * 1e9));
+            CKL();
+            h->launches++;
+            int one = 1;
+            CK(cudaMemcpyAsync(&h->ctrl->has_deadline, &one, sizeof(int), cudaMemcpyHostToDevice, s));
         }
         if (use_eager(h, B)) {
             st->loop_seconds = run_eager<T>(h, B);
@@ -1157,17 +1212,50 @@ void check_plan(const Plan& p, long long rows, long long nnz, bool panels) {
 }
 
 // host tile plan from the device indptr, then the chunk run flags on device
+// Row panels for A x~ (hpr_spmv.cuh): measured per launch of the F product,
+// chunk tiles vs row panels (tools/gpu_r2k.sh) -- C4 (25.7M entries in F,
+// ~28-row groups): 56.3 vs 65.3 us; C5 (382M, 32-row groups): 622.4 vs
+// 583.9 us.  The x~ reuse pays only once the dense block dominates F and the
+// groups are full, so they are used from RP_MIN_NNZ entries of F on;
+// HPR_ROWPANELS=0/1 forces the choice.
+constexpr long long RP_MIN_NNZ = 100000000LL;
+static bool row_panels_on(long long f_nnz) {
+    static const int mode = [] {
+        const char* e = getenv("HPR_ROWPANELS");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return mode < 0 ? f_nnz >= RP_MIN_NNZ : mode == 1;
+}
+
 void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
-                const int2* d_pinfo = nullptr) {
+                const int2* d_pinfo = nullptr, const int* d_rbase = nullptr) {
     cudaStream_t s = h->stream;
     std::vector<int32_t> ptr(rows + 1);
     std::vector<int2> pinfo(d_pinfo ? rows : 0);
+    std::vector<int32_t> rbh(d_rbase ? rows : 0);
     CK(cudaMemcpyAsync(ptr.data(), M.ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost, s));
     if (d_pinfo && rows)
         CK(cudaMemcpyAsync(pinfo.data(), d_pinfo, sizeof(int2) * rows, cudaMemcpyDeviceToHost, s));
+    if (d_rbase && rows)
+        CK(cudaMemcpyAsync(rbh.data(), d_rbase, sizeof(int) * rows, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    Plan pl = build_tiles(ptr.data(), rows, d_pinfo ? pinfo.data() : nullptr);
+    Plan pl = build_tiles(ptr.data(), rows, d_pinfo ? pinfo.data() : nullptr,
+                          d_rbase ? rbh.data() : nullptr);
     check_plan(pl, rows, std::max<long long>(nnz, 1), &M == &h->FT || &M == &h->AT);
+    M.ngroups = (int)pl.groups.size();
+    M.group_nnz = 0;
+    if (!pl.groups.empty()) {
+        const TileBound b = tile_bound(rows, std::max<long long>(h->nnz, 1));
+        if (!M.gdesc || pl.groups.size() > b.longs ||
+            pl.nslots > h->nnz / RP_COLS + (long long)b.longs + 1)
+            fail(HPR_ERR_INVALID, "internal: row-panel bound violated");
+        for (const int4& g : pl.groups) M.group_nnz += (long long)g.y * g.w;
+        CK(cudaMemcpyAsync(M.gdesc, pl.groups.data(), sizeof(int4) * pl.groups.size(),
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(M.gslot, pl.gslot.data(), sizeof(int) * pl.gslot.size(),
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(M.gcount, 0, sizeof(int) * pl.groups.size(), s));
+    }
     M.rows = rows;
     M.cols = cols;
     M.nnz = nnz;
@@ -1531,11 +1619,14 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         phase("pad");
 
         // ---- flow panels: F^T drops the dense flow block, read from F instead
-        // (single GPU: a partitioned solve reduces A^T y over ranks before the update)
+        // (partitioned: each rank's panels cover its own flow rows, and the
+        // A^T y partials are all-reduced before the update as without panels)
         long long ft_nnz = h->nnz_f;
-        if (!(flags & HPR_FLAG_NO_PANELS) && !h->comm && h->nf && n && h->nnz_f) {
+        const bool rows_dense = h->nf && n && h->nnz_f;
+        if (rows_dense)      // one consecutive-column run per dense F row (panels, row panels)
             k_dense_rows<<<g32(h->nf), LAYOUT_TPB, 0, s>>>(h->F.ptr, h->F.idx, h->nf,
                                                             PANEL_MIN_ROW, h->rbase);
+        if (!(flags & HPR_FLAG_NO_PANELS) && h->nf && n && h->nnz_f) {
             int* roff = sc.alloc<int>(n);
             CK(cudaMemsetAsync(h->d_dev, 0, 2 * sizeof(unsigned long long), s));
             CK(cudaMemsetAsync(lenbuf + n, 0, sizeof(int), s));
@@ -1573,7 +1664,9 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         // ---- tile schedules (host plan from the device indptr)
         plan_tiles(h, h->A, m, n, nnz);
         plan_tiles(h, h->AT, n, m, nnz);
-        plan_tiles(h, h->F, h->nf, n, f_nnz);
+        plan_tiles(h, h->F, h->nf, n, f_nnz, nullptr,
+                   rows_dense && row_panels_on(f_nnz) && !(flags & HPR_FLAG_NO_RUNS) ? h->rbase
+                                                                               : nullptr);
         plan_tiles(h, h->FT, n, h->nf, ft_nnz, h->panels ? h->pinfo : nullptr);
         {
             const int fm = fused_mode();
@@ -1709,7 +1802,8 @@ int hpr_kkt_residual(hpr_handle* h, const double* x, const double* y, const doub
     CheckColsArgs<double> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
                              h->colpart};
     k_check_cols<double><<<gc, TPB, 0, s>>>(ac);
-    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, gr, h->colpart, gc, h->log, 0);
+    k_controller<<<1, CTRL_TPB, 0, s>>>(h->ctrl, h->rowpart, gr, h->colpart, gc, h->log, 0,
+                                        nullptr);
     CKL();
     read_ctrl(h);
     std::memcpy(out, h->h_ctrl->cur, sizeof(hpr_kkt));
@@ -1871,7 +1965,8 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out) {
     out->fused = h->fused ? 1 : 0;
     out->f_nnz = h->F.nnz;
     out->ft_nnz = h->FT.nnz;
-    out->index_free_nnz_f = h->F.free_nnz;
+    out->index_free_nnz_f = h->F.free_nnz + h->F.group_nnz;
+    out->row_panel_groups = h->F.ngroups;
     API_END
 }
 
@@ -1891,6 +1986,8 @@ int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_sta
     c.has_deadline = 0;
     if (tolerance > 0) c.tol = tolerance;
     c.cond = 0;
+    c.halt = 0;
+    c.skipped = 0;
     CK(cudaMemcpyAsync(h->ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     *h->h_ctrl = c;
     if (c.status != -1) st->loop_seconds = 0.0;
@@ -1947,10 +2044,17 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
                 launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, false>{df, nullptr}, s);
                 break;
             }
-            default: enqueue_check<T>(h, p, 1, s); break;
+            default:
+                // the previous check (or the solve's last one) may have set halt
+                CK(cudaMemsetAsync(&h->ctrl->halt, 0, sizeof(int), s));
+                enqueue_check<T>(h, p, 1, s);
+                break;
         }
         CKL();
     };
+    // a finished solve leaves Ctrl::halt set; the loop kernels timed here
+    // must not take their halted (no-op) path
+    CK(cudaMemsetAsync(&h->ctrl->halt, 0, sizeof(int), s));
     auto run = [&]() {
         if (h->last_prec == HPR_FP32) body(float(0));
         else body(double(0));

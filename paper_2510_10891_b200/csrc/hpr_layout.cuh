@@ -156,7 +156,7 @@ __global__ void k_chunk_aux(const int4* tiles, int ntiles, const int* idx, int2*
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (t >= ntiles) return;
     const int4 tl = tiles[t];
-    if (tl.y < 0) {
+    if (tl.y < 0 || tl.x < 0) {          // stream / panel / row-panel tiles
         if (lane == 0) taux[t] = make_int2(0, 0);
         return;
     }

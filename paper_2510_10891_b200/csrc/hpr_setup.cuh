@@ -259,7 +259,11 @@ constexpr int CTRL_TPB = 512;
 
 __global__ void __launch_bounds__(CTRL_TPB)
 k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int nc, LogRec* log,
-             int mode) {
+             int mode, const int* tflag) {
+    if (mode == 1 && c->halt) {                // a queued block after the stop: no-op
+        if (threadIdx.x == 0) c->skipped = 1;
+        return;
+    }
     __shared__ double sums[KR + KC];
     __shared__ double w[KR + KC][CTRL_TPB / 32];
     // all KR + KC slot arrays in one pass (loads of every array in flight
@@ -297,12 +301,14 @@ k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int 
     const double s_lo = sums[KR + 3], s_up = sums[KR + 4], s_dx = sums[KR + 5], nf_x = sums[KR + 6];
 
     if (mode == 1) {
+        c->skipped = 0;
         const long long tnow = c->total + c->B;
         c->total = tnow;
         c->flag_improved = 0;
         c->flag_restart = 0;
         if (nf_y + nf_x > 0.0) {               // hprlp.py:406-409
             c->status = HPR_NUMERICAL_FAILURE;
+            c->halt = 1;
             if (c->cond) cudaGraphSetConditional(c->cond, 0);
             return;
         }
@@ -400,10 +406,17 @@ k_controller(Ctrl* c, const double* rowpart, int nr, const double* colpart, int 
     c->flag_restart = restart;
     if (c->status == -1) {                                     // :394-399
         if (tnow + c->B > c->max_iter) c->status = HPR_ITERATION_LIMIT;
-        else if (c->has_deadline && globaltimer() > c->deadline_ns) c->status = HPR_TIME_LIMIT;
+        else if (tflag ? *tflag != 0 : (c->has_deadline && globaltimer() > c->deadline_ns))
+            c->status = HPR_TIME_LIMIT;        // partitioned: the MAX-reduced flag of all ranks
     }
-    if (c->cond)
-        cudaGraphSetConditional(c->cond, (c->status == -1 && !c->sigma_pending) ? 1u : 0u);
+    c->halt = (c->status != -1 || c->sigma_pending) ? 1 : 0;
+    if (c->cond) cudaGraphSetConditional(c->cond, c->halt ? 0u : 1u);
+}
+
+// partitioned loop: this rank's wall-clock verdict, MAX-reduced over the ranks
+// before the controller reads it (so every rank stops at the same check)
+__global__ void k_deadline_flag(const Ctrl* c, int* flag) {
+    *flag = (!c->halt && c->has_deadline && globaltimer() > c->deadline_ns) ? 1 : 0;
 }
 
 // best-triple save and restart copies (hprlp.py:172-181, 422-424, 430)
@@ -412,6 +425,7 @@ __global__ void k_restart_copy(const Ctrl* c, int n, int m, int nf, const double
                                const double* YM, const double* ZM, double* BXm, double* BYm,
                                double* BZm, T* X, T* Y, T* Z, T* AX, T* AY, T* AZ, const T* BX,
                                const T* BY, const T* BZ, T* YF, const T* BYF) {
+    if (c->skipped) return;
     const int imp = c->flag_improved, rst = c->flag_restart;
     if (!imp && !rst) return;
     const int len = n > m ? n : m;

@@ -74,6 +74,7 @@ __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
+    if (a.ctrl->halt) return;
     const int j = blockIdx.x * TPB + threadIdx.x;
     if (j < a.n) primal_col<T, CHECK>(a, j, a.aty[j]);
 }
@@ -85,6 +86,7 @@ template <typename T, bool CHECK>
 struct EpiPrimal {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
+    static constexpr bool ROW_PANELS = false, COL_PANELS = true;  // F^T only
     PrimalArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { primal_col<T, CHECK>(a, r, s); }
@@ -129,6 +131,7 @@ __device__ __forceinline__ DualRow<T> dual_row(T y, T rhs, T ay, T ax, bool ineq
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
+    if (a.ctrl->halt) return;
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i >= a.m) return;
     const double td = halpern_t(a.ctrl, a.j_in_block);
@@ -169,6 +172,7 @@ template <typename T, bool CHECK>
 struct EpiDual {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
+    static constexpr bool ROW_PANELS = true, COL_PANELS = false;  // F only
     DualArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int f, T s, Acc<0>&) {

@@ -275,11 +275,15 @@ class LpArrays:
 # model) produce bit-identical PTDF rows, hence identical LPs (digests), which
 # is what lets the committed reference trajectories be replayed on the box.
 PTDF_BLAS_THREADS = 8
+# ...and every other BLAS call of a named-config build (the flow rows' base
+# dot products, 13,659-long at C4, are threaded by OpenBLAS above 10^4
+# entries) under a pool of this size
+BUILD_BLAS_THREADS = 2
 
 
-def _blas_pool():
+def _blas_pool(n=None):
     from threadpoolctl import threadpool_limits
-    return threadpool_limits(PTDF_BLAS_THREADS)
+    return threadpool_limits(PTDF_BLAS_THREADS if n is None else n)
 
 
 def _ptdf_full_reference(n_b, fb, tb, react, ref, skip=None):
@@ -829,6 +833,11 @@ def build_config(name: str, n_triples: int | None = None, ptdf_method: str | Non
     (``PTDF_BLAS_THREADS``) unless `device` is given explicitly, so the LP is
     bit-identical wherever it is built; tests/golden/*_trajectory.json and
     c4_window.json carry the digests the GPU parity tests assert."""
+    with _blas_pool(BUILD_BLAS_THREADS):
+        return _build_config(name, n_triples, ptdf_method, device, seed)
+
+
+def _build_config(name, n_triples, ptdf_method, device, seed):
     cfg = dict(CONFIGS[name])
     if seed is not None:
         cfg["seed"] = seed

@@ -371,6 +371,41 @@ def test_partitioned_engine_single_rank(H):
     assert r_tl.status.value == "time-limit"
 
 
+def test_partitioned_engine_single_rank_panels_queue(H):
+    """Partitioned mode on C2 + 500 triples at one rank: flow panels live in
+    the rank's F^T, blocks queued 8 at a time behind the device-side halt
+    flag (host sigma updates in between), same trajectory as the single-GPU
+    solve to FP64 reassociation (the partitioned row-side sums use a fixed
+    slot count)."""
+    import os
+    import torch.distributed as dist
+    from paper_2510_10891_b200 import scuc
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29614")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        doc, mon, lpa = scuc.build_config("C2", n_triples=500)
+        lp = lpa.to_lp()
+        cfg = H.SolverConfig(tolerance=1e-4, ruiz=False, log_residuals=True)
+        ref = H.solve(lp, cfg)
+        comm = H.NcclComm()
+        try:
+            eng = H.Engine(lp, comm=comm)
+            lay = eng.layout()
+            eng.close()
+            r = H.solve_partitioned(lp, cfg, comm=comm)
+        finally:
+            comm.close()
+    finally:
+        dist.destroy_process_group()
+    assert lay["panel_nnz"] > 0
+    assert r.status.value == ref.status.value == "optimal-tolerance"
+    assert (r.iterations, r.restarts) == (ref.iterations, ref.restarts)
+    assert abs(r.objective - ref.objective) <= 1e-9 * abs(ref.objective)
+    a, b = golden_io.log_rows(r), golden_io.log_rows(ref)
+    assert golden_io.trajectory_diff(a, b)["max_row_rel"] <= 1e-8
+
+
 def _edge_lp(kind, seed=5):
     rng = np.random.default_rng(seed)
     n, m = 18, 12

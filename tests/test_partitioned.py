@@ -128,3 +128,24 @@ def test_two_rank_gloo_matches_single_process(cfg_kw, seed):
     y = np.empty(lp.n_rows)
     y[rows0], y[rows1] = a["y"], b["y"]
     assert O.kkt(O.Problem.from_lp(lp), a["x"], y, a["z"]).max_rel <= cfg_kw["tolerance"] * 1.001
+
+
+@pytest.mark.gpu
+def test_partitioned_engine_multi_rank_cuda():
+    """The CUDA partitioned engine (libhprlp_b200.so, NCCL inside the block
+    graph) on >= 2 ranks / GPUs, launched by torchrun: the partitioned solve
+    matches the single-GPU solve and every rank returns the same result
+    (tools/partitioned_check.py).  Skipped on a one-GPU box; the driver's
+    multi-GPU run executes it."""
+    import subprocess
+    import sys
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip(f"needs >= 2 GPUs (this box has {n})")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                          "--local-addr", "127.0.0.1", f"--nproc-per-node={min(n, 4)}",
+                          os.path.join(root, "tools", "partitioned_check.py")],
+                         capture_output=True, text=True, timeout=1200, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
