@@ -804,7 +804,8 @@ template <typename T>
 void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     double* pd = (double*)h->P;
     EpiStore<double> st{pd, nullptr};
-    const int* halt = mode == 1 ? &h->ctrl->halt : nullptr;
+    // the halt flag gates the loop kernels of the queued (partitioned / plain) loop only
+    const int* halt = mode == 1 && (h->comm || plain_graph()) ? &h->ctrl->halt : nullptr;
     launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s,
                 (const double*)nullptr, halt);
     // partitioned: every rank uses the same slot count so the row-side sums reduce slot-wise
@@ -839,28 +840,32 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
 
 template <typename T, bool CHECK>
 void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s) {
+    // the halt flag gates the loop kernels of the queued (partitioned / plain) loop only;
+    // the conditional WHILE node stops the single-GPU loop without it
+    const int* halt = h->comm || plain_graph() ? &h->ctrl->halt : nullptr;
     if (h->fused) {
         // small LPs: the row-wise updates ride on the products' epilogues (2 kernels)
         PrimalArgs<T> pa{h->ctrl, j, h->n, nullptr, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo,
                          p.up, p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
         launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, EpiPrimal<T, CHECK>{pa, nullptr}, s,
-                    p.f_vals, &h->ctrl->halt);
+                    p.f_vals, halt);
         DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, nullptr, p.Y, p.AY, p.rhs, p.YF,
                        p.BY, p.BYF, h->YM, h->YMF, h->rs, h->frow};
         launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, EpiDual<T, CHECK>{da, nullptr}, s,
-                    (const T*)nullptr, &h->ctrl->halt);
+                    (const T*)nullptr, halt);
         return;
     }
     EpiStore<T> st{p.P, nullptr};
-    const int* halt = &h->ctrl->halt;
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals, halt);       // A^T y
     allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
     PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
                      p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
+    pa.halt = halt;
     launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
     launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s, (const T*)nullptr, halt);  // A x~
     DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                    p.BY, p.BYF, h->YM, h->YMF, h->rs};
+    da.halt = halt;
     launch(k_update_dual<T, CHECK>, nblk(h->m), TPB, s, da);
     h->launches += 2;
 }

@@ -44,6 +44,7 @@ struct PrimalArgs {
     // of this pass); hpr_iterate (the single-step API, whose caller sees z)
     // keeps it.
     bool upd_z;
+    const int* halt = nullptr;  // queued block loop only (Ctrl::halt)
 };
 
 template <typename T, bool CHECK>
@@ -74,7 +75,7 @@ __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_primal(PrimalArgs<T> a) {
-    if (a.ctrl->halt) return;
+    if (a.halt && *a.halt) return;
     const int j = blockIdx.x * TPB + threadIdx.x;
     if (j < a.n) primal_col<T, CHECK>(a, j, a.aty[j]);
 }
@@ -113,6 +114,7 @@ struct DualArgs {
     double *YM, *YMF;           // CHECK: master bar y and its folded form
     const double* RS;
     const int* frow;            // nf + 1 folded-row starts (EpiDual)
+    const int* halt = nullptr;  // queued block loop only (Ctrl::halt)
 };
 
 template <typename T>
@@ -131,7 +133,7 @@ __device__ __forceinline__ DualRow<T> dual_row(T y, T rhs, T ay, T ax, bool ineq
 
 template <typename T, bool CHECK>
 __global__ void __launch_bounds__(TPB) k_update_dual(DualArgs<T> a) {
-    if (a.ctrl->halt) return;
+    if (a.halt && *a.halt) return;
     const int i = blockIdx.x * TPB + threadIdx.x;
     if (i >= a.m) return;
     const double td = halpern_t(a.ctrl, a.j_in_block);

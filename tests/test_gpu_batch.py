@@ -36,3 +36,21 @@ def test_solve_many_warm_starts_and_edges():
     assert hprlp.solve_many([], cfg) == []
     with pytest.raises(ValueError):
         hprlp.solve_many(lps, cfg, starts=starts[:1])
+
+
+def test_solve_many_duplicate_entries_get_private_engines():
+    """The same LP object twice (and a second LP sharing its matrix and
+    vectors, e.g. two warm starts of one node LP): every entry gets its own
+    engine -- one handle is never driven by two threads -- and each result
+    equals a lone solve (shared engine_for cache)."""
+    import torch
+    from paper_2510_10891_b200 import hprlp
+    lp = golden_io.random_lps()[5][0]
+    cfg = hprlp.SolverConfig(tolerance=1e-7)
+    ref = hprlp.solve(lp, cfg)
+    dev = torch.cuda.current_device()
+    out = hprlp.solve_many([lp, lp, lp, lp], cfg, workers=4)
+    assert torch.cuda.current_device() == dev
+    for r in out:
+        assert r.iterations == ref.iterations and r.objective == ref.objective
+        assert r.x.tobytes() == ref.x.tobytes()

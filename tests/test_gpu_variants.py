@@ -50,3 +50,49 @@ def test_launch_variants_bit_identical():
     assert _digest({"HPR_EAGER": "1", "HPR_FUSED": "0"}) == base
     assert _digest({"HPR_FUSED": "1"}) == base
     assert _digest({"HPR_FUSED": "1", "HPR_EAGER": "1"}) == base
+
+
+ROWPANEL_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2510_10891_b200 import hprlp, scuc
+doc, mon, lpa = scuc.build_config("C3", n_triples=600)     # ~17 dense flow rows per period
+lp = lpa.to_lp()
+eng = hprlp.Engine(lp)
+groups = eng.layout()["row_panel_groups"]
+rng = np.random.default_rng(5)
+v = rng.standard_normal(lpa.shape[1])
+mv = eng.matvec(v)
+cfg = hprlp.SolverConfig(tolerance=1e-6, ruiz=False, max_iterations=4000, log_residuals=True)
+x, y, z, st, log = eng.solve_raw(cfg)
+print("OUT", json.dumps({"groups": groups, "it": st.iterations, "restarts": st.restarts,
+                         "obj": float(np.dot(lpa.cost, x)), "mv": mv.tolist()[:64],
+                         "mvn": float(np.linalg.norm(mv - lpa.csr() @ v)),
+                         "log": [[r.rel_primal, r.rel_dual, r.rel_gap] for r in log]}))
+""" % ROOT
+
+
+def _rowpanel_run(flag):
+    e = dict(os.environ, HPR_ROWPANELS=flag, HPR_FUSED="0")
+    out = subprocess.run([sys.executable, "-c", ROWPANEL_SCRIPT], env=e, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    import json
+    return json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("OUT")][-1][4:])
+
+
+def test_row_panels_match_chunk_tiles():
+    """Row panels (A x~ over dense flow-row groups, x~ read once per slab; on
+    by default from 100M entries of F, i.e. C5) forced on a C3 LP against the
+    per-row chunk tiles: the product equals scipy to 1e-13 relative and the
+    solve follows the same trajectory to FP64 reassociation."""
+    a, b = _rowpanel_run("0"), _rowpanel_run("1")
+    assert a["groups"] == 0 and b["groups"] > 0
+    import numpy as np
+    scale = max(1.0, float(np.abs(a["mv"]).max()))
+    assert b["mvn"] <= 1e-12 * scale * 100 and a["mvn"] <= 1e-12 * scale * 100
+    assert (a["it"], a["restarts"]) == (b["it"], b["restarts"])
+    assert abs(a["obj"] - b["obj"]) <= 1e-9 * abs(a["obj"])
+    la, lb = np.array(a["log"]), np.array(b["log"])
+    assert np.max(np.abs(la - lb) / np.maximum(la.max(axis=1, keepdims=True), 1e-300)) <= 1e-8

@@ -132,6 +132,15 @@ def test_device_flows_and_resident_tables():
                                    atol=1e-12 * max(1.0, np.abs(want).max()))
     info = scr.info()
     assert info["n_tables"] == 13 and info["bus_pitch"] % 16 == 0
+    # a closed screen is dead and out of the cache (use after free)
+    scr.close()
+    with pytest.raises(ValueError):
+        scr.run(inj, tol)
+    scr2 = screen.screen_for(ptdf, inst)
+    assert scr2 is not scr and scr2.handle is not None
+    scr2.run(inj, tol)
+    np.testing.assert_allclose(scr2.flows(0), g["c3_tables"][0] @ inj, rtol=0,
+                               atol=1e-12 * max(1.0, np.abs(g["c3_tables"][0] @ inj).max()))
 
 
 @pytest.mark.gpu

@@ -41,6 +41,28 @@ inst = parse_instance(doc)
 if a.backend == "gpu":
     from paper_2510_10891_b200 import hprlp
     hprlp.install()
+
+# wall time of the driver's per-pass model construction (driver.py:210, :249-250)
+# and of every LP solve, whichever backend is bound
+_timed = {"compute_ptdf_s": [], "build_model_s": [], "lp_solve_s": []}
+
+
+def _wrap(mod, name, key):
+    fn = getattr(mod, name)
+
+    def timed(*args, **kw):
+        t = time.perf_counter()
+        try:
+            return fn(*args, **kw)
+        finally:
+            _timed[key].append(time.perf_counter() - t)
+    setattr(mod, name, timed)
+
+
+import scuckit.hprlp  # noqa: E402
+_wrap(driver, "compute_ptdf", "compute_ptdf_s")
+_wrap(driver, "build_model", "build_model_s")
+_wrap(scuckit.hprlp, "solve", "lp_solve_s")
 t0 = time.perf_counter()
 rep = driver.run(inst, driver.DriverConfig(time_limit=a.time_limit))
 wall = time.perf_counter() - t0
@@ -50,7 +72,9 @@ out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown
        "wall_s": wall, "status": d["status"], "exit_code": d["exit_code"],
        "objective": d["objective"], "timings": d["timings"], "nodes_total": d["nodes_total"],
        "fixing": d["fixing"], "passes": d["passes"], "monitored_rows": len(d["monitored"]),
-       "host_cores": os.cpu_count()}
+       "host_cores": os.cpu_count(),
+       "compute_ptdf_s": _timed["compute_ptdf_s"], "build_model_s": _timed["build_model_s"],
+       "lp_solves": len(_timed["lp_solve_s"]), "lp_solve_s_total": sum(_timed["lp_solve_s"])}
 line = json.dumps(out)
 print(line, flush=True)
 if a.out:
