@@ -148,14 +148,14 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel_key):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture summary (profiles/ncu_traffic.json), or None."""
+def ncu_traffic(kernel_key, config):
+    """Per-launch DRAM bytes of the dominant kernel on this config from the
+    committed ncu capture summary (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(kernel_key)
+        return d.get(config, {}).get(kernel_key)
     except Exception:
         return None
 
@@ -375,7 +375,7 @@ def run_b200(args):
     dom = max(ktimes, key=ktimes.get)
     dom_t, dom_b = ktimes[dom], stored[dom]
     ach = dom_b / dom_t / 1e9
-    traffic = ncu_traffic(f"{dom}_{args.precision}")
+    traffic = ncu_traffic(f"{dom}_{args.precision}", args.config)
     it_gbs = bm["iter"] * its / t_loop / 1e9
 
     out = {
