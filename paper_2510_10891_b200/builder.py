@@ -25,6 +25,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import scuc
+from .lp import lazy_csc_matrix
 
 
 class _TableRows:
@@ -95,7 +96,7 @@ def build_model(instance, monitored=(), ptdf=None):
     lpa = scuc.build_relaxation(arrays, monitored,
                                 ptdf=_TableRows(ptdf) if monitored else None)
     csr = sp.csr_matrix((lpa.data, lpa.indices, lpa.indptr), shape=lpa.shape)
-    lp = K.StandardFormLp(matrix=K.SparseMatrix(csr), rhs=lpa.rhs, cost=lpa.cost,
+    lp = K.StandardFormLp(matrix=lazy_csc_matrix(K.SparseMatrix, csr), rhs=lpa.rhs, cost=lpa.cost,
                           lower=lpa.lower, upper=lpa.upper, n_eq=lpa.n_eq,
                           row_tags=_row_tags(instance, monitored),
                           col_tags=_col_tags(instance, vmap))

@@ -111,3 +111,51 @@ class MilpModel:
         return StandardFormLp(lp.matrix, lp.rhs.copy(), lp.cost.copy(), lp.lower.copy(),
                               lp.upper.copy(), lp.n_eq, lp.offset, list(lp.row_tags),
                               list(lp.col_tags))
+
+
+_LAZY_CLASSES: dict = {}
+
+
+def lazy_csc_matrix(cls, matrix):
+    """An instance of ``cls`` -- the caller's ``SparseMatrix`` class, the
+    reference's after ``install()`` -- holding the canonical CSR of `matrix`
+    and building its CSC copy (and the CSR view of A^T) on first use.
+
+    The reference's constructor converts to CSC eagerly
+    (``lp_kernel.py:52-62``); the drop-in's model builder and presolve build
+    large reduced models every fixing round, and the GPU engine only reads
+    ``.csr`` (it transposes on the device), so the CSC conversion -- a few
+    seconds at C4 -- is deferred until a CPU code path asks for it.  The
+    object is an instance of ``cls`` and every attribute keeps its meaning;
+    the CSC copy, when built, is the one ``cls`` would have built."""
+    if cls is SparseMatrix:
+        return SparseMatrix(matrix)
+    sub = _LAZY_CLASSES.get(cls)
+    if sub is None:
+        def __init__(self, m, dtype=np.float64):
+            import scipy.sparse as sp
+            csr = sp.csr_matrix(m, dtype=dtype)
+            csr.sum_duplicates()
+            csr.eliminate_zeros()
+            csr.sort_indices()
+            self.csr = csr
+            self.shape = csr.shape
+            self.dtype = csr.dtype
+
+        def _csc(self):
+            c = self.__dict__.get("_lazy_csc")
+            if c is None:
+                c = self.csr.tocsc()
+                c.sort_indices()
+                self.__dict__["_lazy_csc"] = c
+            return c
+
+        sub = type(cls.__name__, (cls,), {
+            "__init__": __init__,
+            "csc": property(_csc),
+            "_t": property(lambda self: _csc(self).T),
+            "__module__": cls.__module__,
+            "__doc__": cls.__doc__,
+        })
+        _LAZY_CLASSES[cls] = sub
+    return sub(matrix)

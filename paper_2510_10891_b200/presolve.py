@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _capi
+from .lp import lazy_csc_matrix
 
 _FIXED_TOL = 1e-10        # presolve.py:24
 _MAX_PASSES = 100         # presolve.py:195
@@ -187,7 +188,7 @@ def milp_presolve(model):
     log.objective_delta = float(red.cost[fixed] @ fixed_at[fixed])
     shift = (red.csr @ np.where(fixed, fixed_at, 0.0)) if fixed.any() else np.zeros(lp.n_rows)
     reduced_lp = type(lp)(
-        matrix=type(lp.matrix)(red.csr[rows][:, cols]),
+        matrix=lazy_csc_matrix(type(lp.matrix), red.csr[rows][:, cols]),
         rhs=(red.rhs - shift)[rows],
         cost=red.cost[cols].copy(),
         lower=red.lower[cols],
@@ -213,7 +214,7 @@ def lp_presolve(lp):
     rows = np.flatnonzero(red.alive_row)
     log.kept_rows = rows.astype(np.int64)
     reduced = type(lp)(
-        matrix=type(lp.matrix)(red.csr[rows]),
+        matrix=lazy_csc_matrix(type(lp.matrix), red.csr[rows]),
         rhs=red.rhs[rows],
         cost=red.cost.copy(),
         lower=red.lower,
