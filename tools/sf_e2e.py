@@ -44,7 +44,8 @@ if a.backend == "gpu":
 
 # wall time of the driver's per-pass model construction (driver.py:210, :249-250)
 # and of every LP solve, whichever backend is bound
-_timed = {"compute_ptdf_s": [], "build_model_s": [], "lp_solve_s": []}
+_timed = {"compute_ptdf_s": [], "build_model_s": [], "lp_solve_s": [], "screen_s": [],
+          "violations": [], "model_nnz": []}
 
 
 def _wrap(mod, name, key):
@@ -63,8 +64,38 @@ import scuckit.hprlp  # noqa: E402
 _wrap(driver, "compute_ptdf", "compute_ptdf_s")
 _wrap(driver, "build_model", "build_model_s")
 _wrap(scuckit.hprlp, "solve", "lp_solve_s")
+_wrap(driver, "screen_violations", "screen_s")
+_bm, _sv = driver.build_model, driver.screen_violations
+
+
+def _bm_count(*args, **kw):
+    out = _bm(*args, **kw)
+    _timed["model_nnz"].append(int(out[0].lp.matrix.csr.nnz))
+    return out
+
+
+def _sv_count(*args, **kw):
+    out = _sv(*args, **kw)
+    _timed["violations"].append(len(out))
+    return out
+
+
+driver.build_model, driver.screen_violations = _bm_count, _sv_count
 t0 = time.perf_counter()
-rep = driver.run(inst, driver.DriverConfig(time_limit=a.time_limit))
+try:
+    rep = driver.run(inst, driver.DriverConfig(time_limit=a.time_limit))
+except Exception as exc:          # e.g. a pass-2 model beyond int32 indexing
+    wall = time.perf_counter() - t0
+    out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown_feasible,
+           "time_limit_s": a.time_limit, "wall_s": wall,
+           "error": f"{type(exc).__name__}: {exc}", "host_cores": os.cpu_count(),
+           **{k: v for k, v in _timed.items() if k != "lp_solve_s"},
+           "lp_solves": len(_timed["lp_solve_s"]), "lp_solve_s_total": sum(_timed["lp_solve_s"])}
+    print(json.dumps(out), flush=True)
+    if a.out:
+        with open(a.out, "w") as fh:
+            fh.write(json.dumps(out) + "\n")
+    sys.exit(0)
 wall = time.perf_counter() - t0
 d = rep.to_json_dict()
 out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown_feasible,
@@ -74,6 +105,8 @@ out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown
        "fixing": d["fixing"], "passes": d["passes"], "monitored_rows": len(d["monitored"]),
        "host_cores": os.cpu_count(),
        "compute_ptdf_s": _timed["compute_ptdf_s"], "build_model_s": _timed["build_model_s"],
+       "screen_s": _timed["screen_s"], "violations": _timed["violations"],
+       "model_nnz": _timed["model_nnz"],
        "lp_solves": len(_timed["lp_solve_s"]), "lp_solve_s_total": sum(_timed["lp_solve_s"])}
 line = json.dumps(out)
 print(line, flush=True)
