@@ -22,6 +22,7 @@ from tests import golden_io  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default=None)
 ap.add_argument("--c4", action="store_true")
+ap.add_argument("--c4full", action="store_true", help="also the full C4 runs (c4_full_*.json)")
 a = ap.parse_args()
 
 
@@ -72,6 +73,14 @@ if a.c4:
     for prec in ("fp64", "fp32"):
         o = probe("C4-window", lpa, g[prec], prec, max_it=g["max_iterations"])
         res.append(o)
+if a.c4full:
+    doc, mon, lpa = scuc.build_config("C4")
+    for prec in ("fp64", "fp32"):
+        p = os.path.join(golden_io.GOLDEN, f"c4_full_{prec}.json")
+        if os.path.exists(p):
+            g = json.load(open(p))
+            print("C4 full digest", lpa.digest() == g["digest"], flush=True)
+            res.append(probe("C4-full", lpa, g[prec], prec))
 if a.out:
     with open(a.out, "w") as fh:
         json.dump(res, fh, indent=1)
