@@ -336,8 +336,10 @@ def run_b200(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("timed")       # ncu --nvtx-include "timed/" (launch list)
         st = eng.resume(args.steps * BLOCK, tolerance=1e-300)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
         split = {name: eng.bench_kernel(which, args.kernel_reps) for name, which in
                  (("spmv_A", 0), ("spmv_AT", 1), ("update_primal", 2), ("update_dual", 3))}
         fused = bool(lay.get("fused"))

@@ -669,7 +669,8 @@ _BUILDER_SITES = {"build_model": ("scuckit.formulation", "scuckit.driver", "scuc
                                    "scuckit")}
 
 
-def install(module=None, presolve: bool = True, screen: bool = True, builder: bool = True):
+def install(module=None, presolve: bool = True, screen: bool = True, builder: bool = True,
+            bb: bool = True):
     """Route the reference's LP solves to the GPU engine.
 
     Rebinds ``scuckit.hprlp.solve`` (and ``kkt_residual`` / ``hpr_iterate``)
@@ -685,7 +686,10 @@ def install(module=None, presolve: bool = True, screen: bool = True, builder: bo
     (``build_model``, ``driver.py:249-250``; ``compute_ptdf``, ``:210``) is
     rebound to ``builder.py``: the reference's own model objects, built
     vectorised (identical rows, bounds and tags), PTDF tables from one solve
-    plus LODF updates."""
+    plus LODF updates.  With ``bb`` the branch-and-bound's ``_Search``
+    (``milp_bb.py:101-404``) solves a plunge's waiting sibling ahead on a
+    second engine and stream (``bb.py``); every node result, hence the
+    search, is unchanged."""
     import importlib
     if module is None:
         import scuckit.hprlp as module
@@ -719,6 +723,15 @@ def install(module=None, presolve: bool = True, screen: bool = True, builder: bo
             if hasattr(mod, "screen_violations"):
                 _SAVED.setdefault("screen", {}).setdefault(name, mod.screen_violations)
                 mod.screen_violations = dev_screen.screen_violations
+    if bb:
+        from . import bb as spec
+        mbb = importlib.import_module("scuckit.milp_bb")
+        lpb = importlib.import_module("scuckit.lp_backends")
+        if "bb" not in _SAVED:
+            _SAVED["bb"] = (mbb._Search, lpb.solve_lp)
+        mbb._Search = spec.make_search_class(mbb, lpb)
+        if getattr(lpb.solve_lp, "__wrapped__", None) is None:
+            lpb.solve_lp = spec.wrap_solve_lp(lpb.solve_lp)
     if builder:
         from . import builder as fast
         for fn, sites in _BUILDER_SITES.items():
@@ -744,6 +757,10 @@ def uninstall():
         importlib.import_module(name).screen_violations = orig
     for (name, fn), orig in _SAVED.get("builder", {}).items():
         setattr(importlib.import_module(name), fn, orig)
+    if "bb" in _SAVED:
+        search, solve_lp = _SAVED["bb"]
+        importlib.import_module("scuckit.milp_bb")._Search = search
+        importlib.import_module("scuckit.lp_backends").solve_lp = solve_lp
     from . import presolve as native
     native._LOG_CLASS = native.ReductionLog
     from . import screen as dev_screen

@@ -166,3 +166,35 @@ def test_driver_run_completes_like_reference():
         gpu.uninstall()
     _assert_same_run(cpu, g["report"], "reference on the box vs its record")
     _assert_same_run(got, cpu, "B200 path vs reference on the box")
+
+
+def test_speculative_bb_leaves_the_search_unchanged():
+    """bb.py: the plunge's waiting sibling is solved ahead on a second engine
+    and stream; the reference's B&B (milp_bb.py:279-404) must take exactly the
+    same path -- node log, incumbent, bound, node and LP-solve counts -- as
+    with speculation off, and the speculative results must actually be used."""
+    from scuckit import apply_instance_scaling, build_model, parse_instance
+    from scuckit.milp_bb import BbConfig, solve_milp
+    from scuckit.presolve import milp_presolve
+    from paper_2510_10891_b200 import bb, hprlp as gpu, scuc
+    doc = scuc.generate_instance(30, 12, 45, 8, seed=3, shutdown_feasible=True)
+    inst, _ = apply_instance_scaling(parse_instance(doc))
+    out = {}
+    for spec in (False, True):
+        gpu.install(bb=spec)
+        try:
+            model, _ = build_model(inst, monitored=scuc.sample_monitored(doc, 40, 3))
+            red, log = milp_presolve(model)
+            before = dict(bb.STATS)
+            res = solve_milp(red, gap=1e-4, config=BbConfig(node_limit=40))
+            out[spec] = (res, {k: bb.STATS[k] - before[k] for k in bb.STATS})
+        finally:
+            gpu.uninstall()
+    (a, _), (b, st) = out[False], out[True]
+    assert (a.status, a.nodes, a.lp_solves) == (b.status, b.nodes, b.lp_solves)
+    assert a.objective == b.objective or (np.isnan(a.objective) and np.isnan(b.objective))
+    assert a.bound == b.bound
+    assert [(n["node"], n["action"], n["bound"]) for n in a.node_log] == \
+           [(n["node"], n["action"], n["bound"]) for n in b.node_log]
+    print("speculation", st)
+    assert st["speculated"] > 0 and st["hits"] > 0
