@@ -15,7 +15,12 @@ namespace hpr {
 
 constexpr int TPB = 128;          // threads per CTA for every tiled kernel
 constexpr int TILE_NNZ = 1024;    // nonzeros staged per stream tile (8 KB FP64 products; 8 per thread)
-constexpr int TILE_ROWS = TPB;    // rows per stream tile (one epilogue row per thread)
+#ifndef HPR_TILE_ROWS
+#define HPR_TILE_ROWS 128
+#endif
+// rows per stream tile: the short structural rows (3.6 entries on average at C4)
+// fill a 1,024-entry tile only if a tile may hold more rows than threads
+constexpr int TILE_ROWS = HPR_TILE_ROWS;
 constexpr int ITEMS = TILE_NNZ / TPB;
 constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row
 constexpr int MAX_B = 64;         // largest check_every the loop graph holds (longer: eager blocks)

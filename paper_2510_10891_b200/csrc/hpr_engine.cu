@@ -142,7 +142,10 @@ void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&.
 }
 
 // fixed grid of the row-wise passes: deterministic partial-sum slots
-constexpr int ROW_GRID_MAX = 148 * 32;
+#ifndef HPR_ROW_GRID
+#define HPR_ROW_GRID (148 * 32)
+#endif
+constexpr int ROW_GRID_MAX = HPR_ROW_GRID;
 inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 // ===========================================================================

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
             c[q] = e < cnt ? ld_stream(idx + e) : 0;
             v[q] = e < cnt ? ld_stream(val + e) : T(0);
         }
-        if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
+        for (int k = threadIdx.x; k < R; k += TPB) sptr[k] = A.indptr[r0 + k] - p0;
         if (threadIdx.x == 0) sptr[R] = cnt;
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {

@@ -2,7 +2,7 @@
 A=$1; B=$2; R=${3:-3}
 for i in $(seq $R); do
   for L in $A $B; do
-    HPR_LIB=$L timeout 300 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/ab.log 2>&1
+    HPR_LIB=$L timeout 300 python bench.py --no-e2e --no-cpu-baseline --no-screen --steps 30 > gpurun_out/ab.log 2>&1
     python -c "import json,sys;d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]);print('$L'.split('/')[-1], round(d['value'],1), round(d['iteration_us'],1), {k: round(v['us'],1) for k,v in d['kernels'].items()}, round(d['check_block_us'],1))"
   done
 done

@@ -108,6 +108,9 @@ out = {"backend": a.backend, "config": a.config, "shutdown_feasible": a.shutdown
        "screen_s": _timed["screen_s"], "violations": _timed["violations"],
        "model_nnz": _timed["model_nnz"],
        "lp_solves": len(_timed["lp_solve_s"]), "lp_solve_s_total": sum(_timed["lp_solve_s"])}
+if a.backend == "gpu":
+    from paper_2510_10891_b200 import bb
+    out["bb_speculation"] = dict(bb.STATS)
 line = json.dumps(out)
 print(line, flush=True)
 if a.out:
