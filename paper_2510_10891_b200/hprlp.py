@@ -670,7 +670,7 @@ _BUILDER_SITES = {"build_model": ("scuckit.formulation", "scuckit.driver", "scuc
 
 
 def install(module=None, presolve: bool = True, screen: bool = True, builder: bool = True,
-            bb: bool = True):
+            bb: bool = False):
     """Route the reference's LP solves to the GPU engine.
 
     Rebinds ``scuckit.hprlp.solve`` (and ``kkt_residual`` / ``hpr_iterate``)
@@ -686,10 +686,11 @@ def install(module=None, presolve: bool = True, screen: bool = True, builder: bo
     (``build_model``, ``driver.py:249-250``; ``compute_ptdf``, ``:210``) is
     rebound to ``builder.py``: the reference's own model objects, built
     vectorised (identical rows, bounds and tags), PTDF tables from one solve
-    plus LODF updates.  With ``bb`` the branch-and-bound's ``_Search``
-    (``milp_bb.py:101-404``) solves a plunge's waiting sibling ahead on a
-    second engine and stream (``bb.py``); every node result, hence the
-    search, is unchanged."""
+    plus LODF updates.  With ``bb`` (opt-in) the branch-and-bound's
+    ``_Search`` (``milp_bb.py:101-404``) solves a plunge's waiting sibling
+    ahead on a second engine and stream (``bb.py``); every node result, hence
+    the search, is unchanged.  It pays when dives are short and siblings are
+    revisited, and costs GPU time a long dive needs."""
     import importlib
     if module is None:
         import scuckit.hprlp as module

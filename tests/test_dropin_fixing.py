@@ -181,7 +181,7 @@ def test_speculative_bb_leaves_the_search_unchanged():
     inst, _ = apply_instance_scaling(parse_instance(doc))
     out = {}
     for spec in (False, True):
-        gpu.install(bb=spec)
+        gpu.install(bb=spec)            # opt-in (install() leaves the B&B as written)
         try:
             model, _ = build_model(inst, monitored=scuc.sample_monitored(doc, 40, 3))
             red, log = milp_presolve(model)
