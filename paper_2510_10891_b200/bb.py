@@ -96,6 +96,7 @@ def make_search_class(milp_bb, lp_backends):
         def __init__(self, *args, **kw):
             super().__init__(*args, **kw)
             self._spec = {}
+            self._stream = None
             self._pool = ThreadPoolExecutor(max_workers=1)
             import torch
             self._device = torch.cuda.current_device() if torch.cuda.is_available() else None
@@ -124,7 +125,12 @@ def make_search_class(milp_bb, lp_backends):
             if prep is None:
                 return None, None
             lp2, warm = prep
-            eng = hprlp.Engine(lp2, device=self._device)
+            # a default-priority stream: the search's own solves run on the
+            # engine's greatest-priority private streams, so the speculative
+            # work only takes SMs they leave idle
+            if self._stream is None:
+                self._stream = torch.cuda.Stream(device=self._device, priority=0)
+            eng = hprlp.Engine(lp2, device=self._device, stream=self._stream)
             try:
                 res = hprlp._with_fp64_retry(
                     cfg, lambda c, t0: hprlp._solve_once(lp2, c, warm, t0, engine=eng))

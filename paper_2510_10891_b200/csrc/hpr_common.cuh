@@ -21,6 +21,7 @@ constexpr int TILE_NNZ = 1024;    // nonzeros staged per stream tile (8 KB FP64 
 // rows per stream tile: the short structural rows (3.6 entries on average at C4)
 // fill a 1,024-entry tile only if a tile may hold more rows than threads
 constexpr int TILE_ROWS = HPR_TILE_ROWS;
+static_assert(TILE_ROWS == TPB || TILE_ROWS == 2 * TPB, "stream tiles fill sptr in at most two passes");
 constexpr int ITEMS = TILE_NNZ / TPB;
 constexpr int CHUNK_NNZ = TILE_NNZ;  // nonzeros per CTA on a long (split) row
 constexpr int MAX_B = 64;         // largest check_every the loop graph holds (longer: eager blocks)

@@ -143,7 +143,7 @@ void launch(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args&&.
 
 // fixed grid of the row-wise passes: deterministic partial-sum slots
 #ifndef HPR_ROW_GRID
-#define HPR_ROW_GRID (148 * 32)
+#define HPR_ROW_GRID (148 * 8)   // A/B (tools/gpu_r2r.sh): check block 216 -> 207 us at C4 vs 148 * 32 slots
 #endif
 constexpr int ROW_GRID_MAX = HPR_ROW_GRID;
 inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
@@ -154,6 +154,7 @@ inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 
 struct Plan {
     std::vector<int4> tiles, longs;
+    std::vector<int4> rtiles;     // row-panel tiles {-(g+1), column tile, 0, 0} (k_spmv_rows)
     std::vector<int4> groups;     // row panels {r0, R, c0, len}
     std::vector<int> gslot;       // first partial slot per group
     long long nslots = 0;         // row-panel partial slots
@@ -184,7 +185,7 @@ Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr,
                 p.groups.push_back(make_int4(r, r1 - r, c0, len));
                 p.gslot.push_back((int)p.nslots);
                 p.nslots += (long long)(r1 - r) * nct;
-                for (int ct = 0; ct < nct; ++ct) p.tiles.push_back(make_int4(-(g + 1), ct, 0, 0));
+                for (int ct = 0; ct < nct; ++ct) p.rtiles.push_back(make_int4(-(g + 1), ct, 0, 0));
                 r = r1;
                 continue;
             }
@@ -274,6 +275,8 @@ struct DevCsr {
     long long free_nnz = 0;      // entries in index-free chunks
     int* counters = nullptr;
     double* tpart = nullptr;
+    int4* rtiles = nullptr;      // row-panel tiles (F only), launched as k_spmv_rows
+    int nrtiles = 0;
     int4* gdesc = nullptr;       // row panels (F only; hpr_common.cuh Csr::gdesc)
     int* gslot = nullptr;
     int* gcount = nullptr;
@@ -390,6 +393,7 @@ size_t carve(hpr_handle* h, char* base) {
         if (&M == &h->F) {
             // row panels: groups of >= RP_MIN_ROWS long rows, so at most one per
             // RP_MIN_ROWS long rows; one partial per row per RP_COLS columns
+            M.rtiles = cv.take<int4>(nnz / RP_COLS + tb.longs + 1);
             M.gdesc = cv.take<int4>(tb.longs);
             M.gslot = cv.take<int>(tb.longs);
             M.gcount = cv.take<int>(tb.longs);
@@ -630,8 +634,18 @@ void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, con
     if (M.pinfo && !pvals) fail(HPR_ERR_INVALID, "internal: panel operand without F values");
     Csr<T> v = M.view<T>(vals, pvals);
     v.halt = halt;
-    launch(k_spmv<T, Epi>, M.ntiles, TPB, s, v, xg, epi);
-    h->launches += 1;
+    if (M.nrtiles) {             // F's dense row groups: their own kernel, rows disjoint
+        if constexpr (Epi::ROW_PANELS) {
+            launch(k_spmv_rows<T, Epi>, M.nrtiles, TPB, s, v, (const int4*)M.rtiles, xg, epi);
+            h->launches += 1;
+        } else {
+            fail(HPR_ERR_INVALID, "internal: row panels on an operand without them");
+        }
+    }
+    if (M.ntiles) {
+        launch(k_spmv<T, Epi>, M.ntiles, TPB, s, v, xg, epi);
+        h->launches += 1;
+    }
 }
 
 // power_method (lp_kernel.py:138-175) on the unfolded FP64 operand pair
@@ -1251,6 +1265,7 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
                           d_rbase ? rbh.data() : nullptr);
     check_plan(pl, rows, std::max<long long>(nnz, 1), &M == &h->FT || &M == &h->AT);
     M.ngroups = (int)pl.groups.size();
+    M.nrtiles = (int)pl.rtiles.size();
     M.group_nnz = 0;
     if (!pl.groups.empty()) {
         const TileBound b = tile_bound(rows, std::max<long long>(h->nnz, 1));
@@ -1263,6 +1278,10 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
         CK(cudaMemcpyAsync(M.gslot, pl.gslot.data(), sizeof(int) * pl.gslot.size(),
                            cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(M.gcount, 0, sizeof(int) * pl.groups.size(), s));
+        if ((long long)pl.rtiles.size() > h->nnz / RP_COLS + (long long)b.longs + 1)
+            fail(HPR_ERR_INVALID, "internal: row-panel tile bound violated");
+        CK(cudaMemcpyAsync(M.rtiles, pl.rtiles.data(), sizeof(int4) * pl.rtiles.size(),
+                           cudaMemcpyHostToDevice, s));
     }
     M.rows = rows;
     M.cols = cols;
@@ -1397,7 +1416,12 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         if (opt && opt->stream) {
             h->stream = (cudaStream_t)opt->stream;
         } else {
-            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            // the private stream gets the device's greatest priority: work a
+            // caller queues on default-priority streams (e.g. speculative
+            // node-LP solves, bb.py) only fills SMs this solve leaves idle
+            int least = 0, greatest = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            CK(cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, greatest));
             h->own_stream = true;
         }
         CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));

@@ -76,77 +76,7 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
     Acc<Epi::K> acc;
     acc.zero();
     const int4 tl = A.tiles[blockIdx.x];
-    if (Epi::ROW_PANELS && tl.x < 0) {
-        // ------- row-panel tile {-(g+1), ct, 0, 0}: RP_COLS columns of a dense row group -------
-        // Each lane holds 4 x~ values of the slab for all the group's rows
-        // (x~ read once per slab, not once per entry as in a chunk tile);
-        // warp w sums rows w, w+4, ... over the slab (coalesced 256-byte row
-        // segments) and stores the slab partial.  The group's last tile adds
-        // each row's partials in slab order -- deterministic.
-        const int g = -tl.x - 1, ct = tl.y;
-        const int4 gd = A.gdesc[g];           // {r0, R, c0, len}
-        const int nct = (gd.w + RP_COLS - 1) / RP_COLS;
-        const int cb = ct * RP_COLS;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        T* __restrict__ gp = reinterpret_cast<T*>(A.gpart) + A.gslot[g];
-        T xv[RP_COLS / 32];
-#pragma unroll
-        for (int q = 0; q < RP_COLS / 32; ++q) {
-            const int c = cb + lane + 32 * q;
-            xv[q] = c < gd.w ? ld_ro(xg + gd.z + c) : T(0);
-        }
-        // two rows per step (8 value loads in flight per lane)
-        constexpr int NW = TPB / 32;
-        for (int r = warp; r < gd.y; r += 2 * NW) {
-            const bool two = r + NW < gd.y;
-            const T* __restrict__ rv0 = A.vals + __ldg(A.indptr + gd.x + r) + cb;
-            const T* __restrict__ rv1 =
-                two ? A.vals + __ldg(A.indptr + gd.x + r + NW) + cb : rv0;
-            T v0[RP_COLS / 32], v1[RP_COLS / 32];
-#pragma unroll
-            for (int q = 0; q < RP_COLS / 32; ++q) {
-                const int c = lane + 32 * q;
-                const bool in = cb + c < gd.w;
-                v0[q] = in ? ld_stream(rv0 + c) : T(0);
-                v1[q] = in && two ? ld_stream(rv1 + c) : T(0);
-            }
-            T s0 = T(0), s1 = T(0);
-#pragma unroll
-            for (int q = 0; q < RP_COLS / 32; ++q) {
-                s0 += v0[q] * xv[q];
-                s1 += v1[q] * xv[q];
-            }
-            s0 = warp_sum(s0);
-            s1 = warp_sum(s1);
-            if (lane == 0) {
-                gp[(size_t)r * nct + ct] = s0;
-                if (two) gp[(size_t)(r + NW) * nct + ct] = s1;
-            }
-        }
-        if (lane == 0) __threadfence();       // this warp's partials before the ticket
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int prev;
-            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                         : "=r"(prev) : "l"(A.gcount + g) : "memory");
-            s_last = (prev == nct - 1);
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();                      // every slab partial of the group is visible
-        if (threadIdx.x == 0) A.gcount[g] = 0;
-        for (int r = warp; r < gd.y; r += TPB / 32) {
-            const volatile T* pr = gp + (size_t)r * nct;
-            T t = T(0);
-            for (int q = lane; q < nct; q += 32) t += pr[q];
-            t = warp_sum(t);
-            if (lane == 0) {
-                Acc<Epi::K> a1;
-                a1.zero();
-                epi.apply(gd.x + r, t, a1);
-            }
-        }
-    } else if (Epi::COL_PANELS && tl.y < 0 && tl.w < 0) {
+    if (Epi::COL_PANELS && tl.y < 0 && tl.w < 0) {
         // ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= TPB rows sharing flow panels -------
         // Remaining (indexed) entries are staged as in a stream tile.  The dense
         // part is read from F's row-major values with thread = F^T row (an F
@@ -216,7 +146,11 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
             c[q] = e < cnt ? ld_stream(idx + e) : 0;
             v[q] = e < cnt ? ld_stream(val + e) : T(0);
         }
-        for (int k = threadIdx.x; k < R; k += TPB) sptr[k] = A.indptr[r0 + k] - p0;
+        // straight-line (a loop here keeps the in-flight loads live across it: spills)
+        if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
+        if constexpr (TILE_ROWS > TPB) {
+            if (threadIdx.x + TPB < R) sptr[threadIdx.x + TPB] = A.indptr[r0 + threadIdx.x + TPB] - p0;
+        }
         if (threadIdx.x == 0) sptr[R] = cnt;
 #pragma unroll
         for (int q = 0; q < ITEMS; ++q) {
@@ -311,6 +245,87 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
 #pragma unroll
                 for (int k = 0; k < Epi::K; ++k) epi.part[(size_t)k * nslots + A.ntiles + li] = a1.v[k];
             }
+        }
+    }
+}
+
+// Row panels of F (A x~ over dense flow-row groups; hpr_common.cuh Csr::gdesc),
+// a kernel of their own launched ahead of k_spmv over F's other tiles (the
+// rows are disjoint): with 8 CTAs/SM it may hold two rows' loads in flight
+// without taking registers from the lean main product.
+template <typename T, class Epi>
+__global__ void __launch_bounds__(TPB, 8) k_spmv_rows(Csr<T> A, const int4* __restrict__ rtiles,
+                                                 const T* __restrict__ xg, Epi epi) {
+    if (A.halt && *A.halt) return;
+    __shared__ int s_last;
+    const int4 tl = rtiles[blockIdx.x];
+    // ------- row-panel tile {-(g+1), ct, 0, 0}: RP_COLS columns of a dense row group -------
+    // Each lane holds 4 x~ values of the slab for all the group's rows
+    // (x~ read once per slab, not once per entry as in a chunk tile);
+    // warp w sums rows w, w+4, ... over the slab (coalesced 256-byte row
+    // segments) and stores the slab partial.  The group's last tile adds
+    // each row's partials in slab order -- deterministic.
+    const int g = -tl.x - 1, ct = tl.y;
+    const int4 gd = A.gdesc[g];           // {r0, R, c0, len}
+    const int nct = (gd.w + RP_COLS - 1) / RP_COLS;
+    const int cb = ct * RP_COLS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T* __restrict__ gp = reinterpret_cast<T*>(A.gpart) + A.gslot[g];
+    T xv[RP_COLS / 32];
+#pragma unroll
+    for (int q = 0; q < RP_COLS / 32; ++q) {
+        const int c = cb + lane + 32 * q;
+        xv[q] = c < gd.w ? ld_ro(xg + gd.z + c) : T(0);
+    }
+    // two rows per step (8 value loads in flight per lane)
+    constexpr int NW = TPB / 32;
+    for (int r = warp; r < gd.y; r += 2 * NW) {
+        const bool two = r + NW < gd.y;
+        const T* __restrict__ rv0 = A.vals + __ldg(A.indptr + gd.x + r) + cb;
+        const T* __restrict__ rv1 =
+            two ? A.vals + __ldg(A.indptr + gd.x + r + NW) + cb : rv0;
+        T v0[RP_COLS / 32], v1[RP_COLS / 32];
+#pragma unroll
+        for (int q = 0; q < RP_COLS / 32; ++q) {
+            const int c = lane + 32 * q;
+            const bool in = cb + c < gd.w;
+            v0[q] = in ? ld_stream(rv0 + c) : T(0);
+            v1[q] = in && two ? ld_stream(rv1 + c) : T(0);
+        }
+        T s0 = T(0), s1 = T(0);
+#pragma unroll
+        for (int q = 0; q < RP_COLS / 32; ++q) {
+            s0 += v0[q] * xv[q];
+            s1 += v1[q] * xv[q];
+        }
+        s0 = warp_sum(s0);
+        s1 = warp_sum(s1);
+        if (lane == 0) {
+            gp[(size_t)r * nct + ct] = s0;
+            if (two) gp[(size_t)(r + NW) * nct + ct] = s1;
+        }
+    }
+    if (lane == 0) __threadfence();       // this warp's partials before the ticket
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(prev) : "l"(A.gcount + g) : "memory");
+        s_last = (prev == nct - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();                      // every slab partial of the group is visible
+    if (threadIdx.x == 0) A.gcount[g] = 0;
+    for (int r = warp; r < gd.y; r += TPB / 32) {
+        const volatile T* pr = gp + (size_t)r * nct;
+        T t = T(0);
+        for (int q = lane; q < nct; q += 32) t += pr[q];
+        t = warp_sum(t);
+        if (lane == 0) {
+            Acc<Epi::K> a1;
+            a1.zero();
+            epi.apply(gd.x + r, t, a1);
         }
     }
 }

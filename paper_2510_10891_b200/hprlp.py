@@ -208,7 +208,7 @@ class Engine:
     the engine's kernels run on a private CUDA stream of the handle."""
 
     def __init__(self, lp, device: int | None = None, reorder: bool = True, fold: bool = True,
-                 runs: bool = True, panels: bool = True, comm=None):
+                 runs: bool = True, panels: bool = True, comm=None, stream=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("the HPR engine needs a CUDA device (no CPU fallback)")
@@ -240,7 +240,11 @@ class Engine:
                  | (0 if panels else _capi.HPR_FLAG_NO_PANELS))
         ncomm, world, rank = (None, 1, 0) if comm is None else (comm.handle, comm.world_size,
                                                                  comm.rank)
-        opt = _capi.Options(dev, None, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
+        # stream: a torch.cuda.Stream to run on (e.g. a low-priority one); None =
+        # a private stream at the device's greatest priority
+        self._stream = stream
+        sp = None if stream is None else _capi.C.c_void_p(stream.cuda_stream)
+        opt = _capi.Options(dev, sp, _capi.C.c_void_p(self._ws.data_ptr()), int(nbytes.value),
                             flags, ncomm, world, rank)
         h = _capi.C.c_void_p()
         _capi.check(self._lib.hpr_create(_capi.C.byref(self._prob), _capi.C.byref(opt),

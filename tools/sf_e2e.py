@@ -28,6 +28,7 @@ ap.add_argument("--backend", choices=["gpu", "cpu"], default="gpu")
 ap.add_argument("--config", default="C1")
 ap.add_argument("--time-limit", type=float, default=1500.0)
 ap.add_argument("--out", default=None)
+ap.add_argument("--bb", action="store_true", help="install(bb=True): speculative sibling solves")
 ap.add_argument("--shutdown-feasible", action="store_true",
                 help="cap initial outputs at the shutdown limit (scuc.generate_instance)")
 a = ap.parse_args()
@@ -40,7 +41,7 @@ doc = scuc.generate_instance(**scuc.CONFIGS[a.config], shutdown_feasible=a.shutd
 inst = parse_instance(doc)
 if a.backend == "gpu":
     from paper_2510_10891_b200 import hprlp
-    hprlp.install()
+    hprlp.install(bb=a.bb)
 
 # wall time of the driver's per-pass model construction (driver.py:210, :249-250)
 # and of every LP solve, whichever backend is bound
