@@ -16,7 +16,7 @@ namespace hpr {
 constexpr int TPB = 128;          // threads per CTA for every tiled kernel
 constexpr int TILE_NNZ = 1024;    // nonzeros staged per stream tile (8 KB FP64 products; 8 per thread)
 #ifndef HPR_TILE_ROWS
-#define HPR_TILE_ROWS 128
+#define HPR_TILE_ROWS 256   // A/B (tools/gpu_r2s.sh): 6,385-6,436 -> 6,550-6,614 it/s at C4 vs 128
 #endif
 // rows per stream tile: the short structural rows (3.6 entries on average at C4)
 // fill a 1,024-entry tile only if a tile may hold more rows than threads
@@ -154,6 +154,10 @@ struct Csr {
 constexpr int RP_ROWS = 32;       // rows per row-panel group
 constexpr int RP_MIN_ROWS = 8;    // fewer dense rows sharing a run: chunk tiles instead
 constexpr int RP_COLS = 128;      // columns per row-panel tile (4 per lane)
+#ifndef HPR_RP_MIN_CTAS
+#define HPR_RP_MIN_CTAS 16
+#endif
+constexpr int RP_MIN_CTAS = HPR_RP_MIN_CTAS;   // k_spmv_rows occupancy target
 
 constexpr int PANEL_ROWS = TPB;   // rows (F^T columns) per panel tile: one per thread
 constexpr int PANEL_MAX_KEEP = 32; // indexed entries a panel row may keep beside its panel

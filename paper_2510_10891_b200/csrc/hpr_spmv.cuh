@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
 // rows are disjoint): with 8 CTAs/SM it may hold two rows' loads in flight
 // without taking registers from the lean main product.
 template <typename T, class Epi>
-__global__ void __launch_bounds__(TPB, 8) k_spmv_rows(Csr<T> A, const int4* __restrict__ rtiles,
+__global__ void __launch_bounds__(TPB, RP_MIN_CTAS) k_spmv_rows(Csr<T> A, const int4* __restrict__ rtiles,
                                                  const T* __restrict__ xg, Epi epi) {
     if (A.halt && *A.halt) return;
     __shared__ int s_last;
