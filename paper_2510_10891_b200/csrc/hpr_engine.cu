@@ -1702,7 +1702,8 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         plan_tiles(h, h->FT, n, h->nf, ft_nnz, h->panels ? h->pinfo : nullptr);
         {
             const int fm = fused_mode();
-            h->fused = !h->comm && (fm == 1 || (fm < 0 && std::max(h->F.ntiles, h->FT.ntiles) <=
+            h->fused = !h->comm && (fm == 1 || (fm < 0 && std::max(h->F.ntiles + h->F.nrtiles,
+                                                                    h->FT.ntiles) <=
                                                               FUSED_MAX_TILES));
         }
         phase("tiles");
