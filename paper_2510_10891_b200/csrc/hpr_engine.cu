@@ -155,6 +155,7 @@ inline int row_grid(long long len) { return std::min(nblk(len), ROW_GRID_MAX); }
 struct Plan {
     std::vector<int4> tiles, longs;
     std::vector<int4> rtiles;     // row-panel tiles {-(g+1), column tile, 0, 0} (k_spmv_rows)
+    std::vector<int4> ptiles;     // F^T panel tiles when they run as k_spmv_panels
     std::vector<int4> groups;     // row panels {r0, R, c0, len}
     std::vector<int> gslot;       // first partial slot per group
     long long nslots = 0;         // row-panel partial slots
@@ -165,7 +166,7 @@ struct Plan {
 // run), runs of >= RP_MIN_ROWS long dense rows over the same column run
 // become row-panel groups instead of per-row chunks.
 Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr,
-                 const int32_t* rb = nullptr) {
+                 const int32_t* rb = nullptr, bool separate_panels = false) {
     Plan p;
     int r = 0;
     auto panel = [&](int q) { return pinfo && pinfo[q].y > 0; };
@@ -201,7 +202,8 @@ Plan build_tiles(const int32_t* ptr, int rows, const int2* pinfo = nullptr,
                 ++r;
             }
             if (r == r0) fail(HPR_ERR_INVALID, "internal: panel row too long");
-            p.tiles.push_back(make_int4(r0, -(r + 1), ptr[r0], -(ptr[r] + 1)));
+            (separate_panels ? p.ptiles : p.tiles)
+                .push_back(make_int4(r0, -(r + 1), ptr[r0], -(ptr[r] + 1)));
             continue;
         }
         if (len > TILE_NNZ) {
@@ -277,6 +279,8 @@ struct DevCsr {
     double* tpart = nullptr;
     int4* rtiles = nullptr;      // row-panel tiles (F only), launched as k_spmv_rows
     int nrtiles = 0;
+    int4* ptiles = nullptr;      // F^T panel tiles launched as k_spmv_panels (large operands)
+    int nptiles = 0;
     int4* gdesc = nullptr;       // row panels (F only; hpr_common.cuh Csr::gdesc)
     int* gslot = nullptr;
     int* gcount = nullptr;
@@ -390,6 +394,7 @@ size_t carve(hpr_handle* h, char* base) {
         M.tpart = cv.take<double>(tb.tiles);
         M.taux = cv.take<int2>(tb.tiles);
         M.pdesc = &M == &h->FT ? cv.take<int4>(tb.tiles) : nullptr;
+        M.ptiles = &M == &h->FT ? cv.take<int4>(tb.tiles) : nullptr;
         if (&M == &h->F) {
             // row panels: groups of >= RP_MIN_ROWS long rows, so at most one per
             // RP_MIN_ROWS long rows; one partial per row per RP_COLS columns
@@ -640,6 +645,15 @@ void launch_spmv(hpr_handle* h, const DevCsr& M, const T* vals, const T* xg, con
             h->launches += 1;
         } else {
             fail(HPR_ERR_INVALID, "internal: row panels on an operand without them");
+        }
+    }
+    if (M.nptiles) {             // F^T's flow panels: their own kernel, rows disjoint
+        if constexpr (Epi::COL_PANELS && Epi::K == 0) {
+            launch(k_spmv_panels<T, Epi>, M.nptiles, TPB, s, v, (const int4*)M.ptiles,
+                   (const int4*)M.pdesc, xg, epi);
+            h->launches += 1;
+        } else {
+            fail(HPR_ERR_INVALID, "internal: panel kernel for this epilogue");
         }
     }
     if (M.ntiles) {
@@ -1241,6 +1255,19 @@ void check_plan(const Plan& p, long long rows, long long nnz, bool panels) {
 // groups are full, so they are used from RP_MIN_NNZ entries of F on;
 // HPR_ROWPANELS=0/1 forces the choice.
 constexpr long long RP_MIN_NNZ = 100000000LL;
+// F^T panel tiles as a kernel of their own (k_spmv_panels: 8 CTAs/SM, 16
+// loads in flight per thread) from this many panel entries on; below it they
+// stay inside the lean k_spmv.  A/B (tools/gpu_r2w.sh): C4 (18.65M panel
+// entries) A^T y 47.2 us inline vs 55.7 as two kernels; C5 (373M) 532.7 vs
+// 488.0 us.  HPR_PANELKERNEL=0/1 forces the choice.
+constexpr long long PANEL_KERNEL_MIN = 100000000LL;
+static bool panel_kernel_on(long long panel_nnz) {
+    static const int mode = [] {
+        const char* e = getenv("HPR_PANELKERNEL");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return mode < 0 ? panel_nnz >= PANEL_KERNEL_MIN : mode == 1;
+}
 static bool row_panels_on(long long f_nnz) {
     static const int mode = [] {
         const char* e = getenv("HPR_ROWPANELS");
@@ -1261,8 +1288,16 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
     if (d_rbase && rows)
         CK(cudaMemcpyAsync(rbh.data(), d_rbase, sizeof(int) * rows, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const bool sep = d_pinfo && panel_kernel_on(h->panel_nnz);
     Plan pl = build_tiles(ptr.data(), rows, d_pinfo ? pinfo.data() : nullptr,
-                          d_rbase ? rbh.data() : nullptr);
+                          d_rbase ? rbh.data() : nullptr, sep);
+    M.nptiles = (int)pl.ptiles.size();
+    if (M.nptiles) {
+        if (!M.ptiles || pl.ptiles.size() > tile_bound(rows, std::max<long long>(nnz, 1), true).tiles)
+            fail(HPR_ERR_INVALID, "internal: panel tile bound violated");
+        CK(cudaMemcpyAsync(M.ptiles, pl.ptiles.data(), sizeof(int4) * pl.ptiles.size(),
+                           cudaMemcpyHostToDevice, s));
+    }
     check_plan(pl, rows, std::max<long long>(nnz, 1), &M == &h->FT || &M == &h->AT);
     M.ngroups = (int)pl.groups.size();
     M.nrtiles = (int)pl.rtiles.size();
@@ -1293,14 +1328,15 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
         CK(cudaMemcpyAsync(M.longs, pl.longs.data(), sizeof(int4) * pl.longs.size(), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(M.counters, 0, sizeof(int) * pl.longs.size(), s));
     }
-    if (d_pinfo && M.ntiles) {
+    const std::vector<int4>& ptl = sep ? pl.ptiles : pl.tiles;   // the list pdesc indexes
+    if (d_pinfo && !ptl.empty()) {
         // panel tiles over one row-major block of F get a direct descriptor
         std::vector<int32_t> rb(h->nf);
         CK(cudaMemcpyAsync(rb.data(), h->rbase, sizeof(int) * h->nf, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        std::vector<int4> pd(M.ntiles, make_int4(0, 0, 0, 0));
-        for (int t = 0; t < M.ntiles; ++t) {
-            const int4 tl = pl.tiles[t];
+        std::vector<int4> pd(ptl.size(), make_int4(0, 0, 0, 0));
+        for (size_t t = 0; t < ptl.size(); ++t) {
+            const int4 tl = ptl[t];
             if (!(tl.y < 0 && tl.w < 0)) continue;
             const int2 pi = pinfo[tl.x];
             const long long stride = pi.y > 1 ? (long long)rb[pi.x + 1] - rb[pi.x] : 1;
@@ -1309,7 +1345,7 @@ void plan_tiles(hpr_handle* h, DevCsr& M, int rows, int cols, long long nnz,
                 uni = (long long)rb[pi.x + q] == (long long)rb[pi.x] + q * stride;
             if (uni) pd[t] = make_int4(pi.x, pi.y, rb[pi.x], (int)stride);
         }
-        CK(cudaMemcpyAsync(M.pdesc, pd.data(), sizeof(int4) * M.ntiles, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(M.pdesc, pd.data(), sizeof(int4) * pd.size(), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
     const bool runs = !(h->flags & HPR_FLAG_NO_RUNS);
@@ -1703,7 +1739,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         {
             const int fm = fused_mode();
             h->fused = !h->comm && (fm == 1 || (fm < 0 && std::max(h->F.ntiles + h->F.nrtiles,
-                                                                    h->FT.ntiles) <=
+                                                                    h->FT.ntiles + h->FT.nptiles) <=
                                                               FUSED_MAX_TILES));
         }
         phase("tiles");

@@ -66,6 +66,64 @@ __device__ __forceinline__ void block_store(Acc<K>& acc, double* part, int nslot
     }
 }
 
+// ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= TPB F^T rows sharing flow panels -------
+// Remaining (indexed) entries are staged as in a stream tile.  The dense part
+// is read from F's row-major values with thread = F^T row (an F column): for
+// every shared flow row i, the tile's threads read one contiguous run of F's
+// row i, y_i and the row's base come from shared memory, and each thread sums
+// its whole column -- no cross-warp reduction, one store per row (A/B at C4
+// shape, tools/flow_probe.cu: 45.0 -> 38.3 us for the flow block against the
+// 32-column tiles with lane = column, warp = every 4th row).  U loads in
+// flight per thread.
+template <typename T, class Epi, int U>
+__device__ __forceinline__ void panel_tile(const Csr<T>& A, int4 tl, int4 pd,
+                                           const T* __restrict__ xg, Epi& epi, T* prod,
+                                           int* sptr, Acc<Epi::K>& acc) {
+    __shared__ T sy[TPB];
+    __shared__ long long sb[TPB];
+    const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = -tl.w - 1 - tl.z;
+    const int R = r1 - r0;
+    {
+        const int* __restrict__ idx = A.indices + p0;
+        const T* __restrict__ val = A.vals + p0;
+        for (int e = threadIdx.x; e < cnt; e += TPB) prod[e] = ld_stream(val + e) * ld_ro(xg + ld_stream(idx + e));
+        if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
+        if (threadIdx.x == 0) sptr[R] = cnt;
+    }
+    const int2 pi = pd.w > 0 ? make_int2(pd.x, pd.y) : A.pinfo[r0];
+    const int k = threadIdx.x;
+    const T* __restrict__ pv = A.pvals + (r0 + k);
+    T s = T(0);
+    for (int q0 = 0; q0 < pi.y; q0 += TPB) {
+        const int nq = min(TPB, pi.y - q0);
+        __syncthreads();               // previous chunk consumed
+        if (threadIdx.x < nq) {
+            const int i = pi.x + q0 + threadIdx.x;
+            sy[threadIdx.x] = ld_ro(xg + i);
+            sb[threadIdx.x] = pd.w > 0 ? (long long)pd.z + (long long)(q0 + threadIdx.x) * pd.w
+                                       : (long long)__ldg(A.rbase + i);
+        }
+        __syncthreads();
+        if (k < R) {
+            int q = 0;
+            for (; q + U <= nq; q += U) {
+                T v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = ld_stream(pv + sb[q + u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) s += v[u] * sy[q + u];
+            }
+            for (; q < nq; ++q) s += ld_stream(pv + sb[q]) * sy[q];
+        }
+    }
+    __syncthreads();                   // staged leftovers visible
+    if (k < R) {
+        T t = T(0);
+        for (int q = sptr[k]; q < sptr[k + 1]; ++q) t += prod[q];
+        epi.apply(r0 + k, t + s, acc);
+    }
+}
+
 template <typename T, class Epi>
 __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* __restrict__ xg, Epi epi) {
     __shared__ T prod[TILE_NNZ];
@@ -77,60 +135,7 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
     acc.zero();
     const int4 tl = A.tiles[blockIdx.x];
     if (Epi::COL_PANELS && tl.y < 0 && tl.w < 0) {
-        // ------- panel tile {r0, -(r1+1), p0, -(p1+1)}: <= TPB rows sharing flow panels -------
-        // Remaining (indexed) entries are staged as in a stream tile.  The dense
-        // part is read from F's row-major values with thread = F^T row (an F
-        // column): for every shared flow row i, the tile's threads read one
-        // contiguous run of F's row i, y_i and the row's base come from shared
-        // memory, and each thread sums its whole column -- no cross-warp
-        // reduction, one store per row (A/B at C4 shape, tools/flow_probe.cu:
-        // 45.0 -> 38.3 us for the flow block against the 32-column tiles
-        // with lane = column, warp = every 4th row).
-        __shared__ T sy[TPB];
-        __shared__ long long sb[TPB];
-        const int r0 = tl.x, r1 = -tl.y - 1, p0 = tl.z, cnt = -tl.w - 1 - tl.z;
-        const int R = r1 - r0;
-        {
-            const int* __restrict__ idx = A.indices + p0;
-            const T* __restrict__ val = A.vals + p0;
-            for (int e = threadIdx.x; e < cnt; e += TPB) prod[e] = ld_stream(val + e) * ld_ro(xg + ld_stream(idx + e));
-            if (threadIdx.x < R) sptr[threadIdx.x] = A.indptr[r0 + threadIdx.x] - p0;
-            if (threadIdx.x == 0) sptr[R] = cnt;
-        }
-        const int4 pd = A.pdesc[blockIdx.x];
-        const int2 pi = pd.w > 0 ? make_int2(pd.x, pd.y) : A.pinfo[r0];
-        const int k = threadIdx.x;
-        const T* __restrict__ pv = A.pvals + (r0 + k);
-        T s = T(0);
-        for (int q0 = 0; q0 < pi.y; q0 += TPB) {
-            const int nq = min(TPB, pi.y - q0);
-            __syncthreads();               // previous chunk consumed
-            if (threadIdx.x < nq) {
-                const int i = pi.x + q0 + threadIdx.x;
-                sy[threadIdx.x] = ld_ro(xg + i);
-                sb[threadIdx.x] = pd.w > 0 ? (long long)pd.z + (long long)(q0 + threadIdx.x) * pd.w
-                                           : (long long)__ldg(A.rbase + i);
-            }
-            __syncthreads();
-            if (k < R) {
-                constexpr int U = 8;
-                int q = 0;
-                for (; q + U <= nq; q += U) {
-                    T v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = ld_stream(pv + sb[q + u]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) s += v[u] * sy[q + u];
-                }
-                for (; q < nq; ++q) s += ld_stream(pv + sb[q]) * sy[q];
-            }
-        }
-        __syncthreads();                   // staged leftovers visible
-        if (k < R) {
-            T t = T(0);
-            for (int q = sptr[k]; q < sptr[k + 1]; ++q) t += prod[q];
-            epi.apply(r0 + k, t + s, acc);
-        }
+        panel_tile<T, Epi, 8>(A, tl, A.pdesc[blockIdx.x], xg, epi, prod, sptr, acc);
         block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
     } else if (tl.y < 0) {
         // ---------------- stream tile {r0, -(r1+1), p0, p1} ----------------
@@ -328,6 +333,30 @@ __global__ void __launch_bounds__(TPB, RP_MIN_CTAS) k_spmv_rows(Csr<T> A, const 
             epi.apply(gd.x + r, t, a1);
         }
     }
+}
+
+// A/B at C5 (tools/gpu_r2w.sh, A^T y): inline 532.7 us; own kernel 16 CTAs/SM x 8 loads
+// 547.0, 12 x 12 529.8, 8 x 16 488.0 (0.98 of the copy peak)
+#ifndef HPR_PANEL_MIN_CTAS
+#define HPR_PANEL_MIN_CTAS 8
+#endif
+#ifndef HPR_PANEL_U
+#define HPR_PANEL_U 16
+#endif
+// The F^T panel tiles of a large operand as a kernel of their own, launched
+// ahead of k_spmv over F^T's other tiles (the rows are disjoint); its launch
+// bounds and batch depth are tuned apart from the lean main product.
+template <typename T, class Epi>
+__global__ void __launch_bounds__(TPB, HPR_PANEL_MIN_CTAS)
+k_spmv_panels(Csr<T> A, const int4* __restrict__ ptiles, const int4* __restrict__ pdesc,
+              const T* __restrict__ xg, Epi epi) {
+    static_assert(Epi::K == 0, "panel kernel: no partial-sum slots");
+    if (A.halt && *A.halt) return;
+    __shared__ T prod[TILE_NNZ];
+    __shared__ int sptr[TPB + 1];
+    Acc<0> acc;
+    panel_tile<T, Epi, HPR_PANEL_U>(A, ptiles[blockIdx.x], pdesc[blockIdx.x], xg, epi, prod, sptr,
+                                    acc);
 }
 
 // out[r] = (A x)[r]

@@ -1,7 +1,8 @@
 """Launch-shape variants of the engine must not change a single bit:
-the eager block loop (HPR_EAGER), the plain host-relaunched graph (HPR_PLAIN)
-and the small-LP fused iteration (HPR_FUSED: the row-wise updates as SpMV
-epilogues) only change how the same operations are scheduled, so the solve output is
+the eager block loop (HPR_EAGER), the plain host-relaunched graph (HPR_PLAIN),
+the small-LP fused iteration (HPR_FUSED: the row-wise updates as SpMV
+epilogues) and the separate F^T panel kernel (HPR_PANELKERNEL) only change how
+the same operations are scheduled, so the solve output is
 compared by digest across fresh processes (the switches are read once per
 process)."""
 
@@ -50,6 +51,10 @@ def test_launch_variants_bit_identical():
     assert _digest({"HPR_EAGER": "1", "HPR_FUSED": "0"}) == base
     assert _digest({"HPR_FUSED": "1"}) == base
     assert _digest({"HPR_FUSED": "1", "HPR_EAGER": "1"}) == base
+    # F^T panel tiles as their own kernel (k_spmv_panels; default from 100M panel
+    # entries): the same tile arithmetic in the same order, so the same bits
+    assert _digest({"HPR_PANELKERNEL": "1", "HPR_FUSED": "0"}) == base
+    assert _digest({"HPR_PANELKERNEL": "1", "HPR_FUSED": "1"}) == base
 
 
 ROWPANEL_SCRIPT = r"""
