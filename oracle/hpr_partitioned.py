@@ -3,18 +3,22 @@
 This restates the reference HPR solve (``scuckit/hprlp.py:332-455``, using
 the same building blocks as ``oracle/hpr_oracle.py``) in the row-partitioned
 form that the multi-GPU engine runs. Each rank owns one
-row block from ``paper_2510_10891_b200.partition``; x, z and the column data
-are replicated on every rank. The collectives are ``torch.distributed``
-all-reduces: gloo in the CPU tests, NCCL in the engine. Every collective of
-the device implementation appears here, in the same place:
+row block from ``paper_2510_10891_b200.partition`` and one slice of the
+columns (chunk = ceil(n / world_size), rank r owns [r·chunk, (r+1)·chunk)).
+The collectives are ``torch.distributed``: gloo in the CPU tests, NCCL in
+the engine. Every collective of the device implementation appears here, in
+the same place:
 
 * scaling: column ∞-norms (MAX), column 1-norms (SUM), ‖rhs‖² (SUM);
 * power method: Aᵀv partials (SUM) and ‖A Aᵀ v‖² (SUM);
-* iteration: the Aᵀy partials (SUM). The primal update is replicated; the
-  A x̃ product and the dual update are local;
-* check: row-side KKT sums (SUM) and the Aᵀ y_m partials (SUM). The column
-  side and the controller are replicated, so every rank takes the same
-  restart / σ / stopping decisions.
+* iteration: the Aᵀy partials are reduce-scattered to the column owners,
+  each rank updates its own x / z slice, and x̃ is all-gathered for the
+  local A x̃ product and dual update;
+* check: the master bar x is all-gathered, the row-side KKT sums (SUM) and
+  the Aᵀ y_m partials (reduce-scatter) are taken, the column-side sums of
+  each slice are all-reduced, and the controller runs replicated on the
+  reduced sums, so every rank takes the same restart / σ / stopping
+  decisions.
 
 ``tests/test_partitioned.py`` runs it with world_size 2 over gloo and
 compares it with the single-process oracle.
@@ -38,6 +42,35 @@ def _allreduce(a: np.ndarray, op=dist.ReduceOp.SUM) -> np.ndarray:
 
 def _allsum(v: float) -> float:
     return float(_allreduce(np.array([v]))[0])
+
+
+def _slice(n: int):
+    ws, r = dist.get_world_size(), dist.get_rank()
+    chunk = -(-n // ws)
+    c0 = min(n, r * chunk)
+    return chunk, c0, min(n, c0 + chunk)
+
+
+def _reduce_scatter(a: np.ndarray) -> np.ndarray:
+    """Sum of the ranks' n-vectors, this rank's owned chunk only."""
+    ws = dist.get_world_size()
+    chunk, c0, c1 = _slice(a.shape[0])
+    full = np.zeros(chunk * ws)
+    full[:a.shape[0]] = a
+    out = torch.zeros(chunk, dtype=torch.float64)
+    dist.reduce_scatter(out, list(torch.from_numpy(full).split(chunk)))
+    return out.numpy()[:c1 - c0]
+
+
+def _all_gather(part: np.ndarray, n: int) -> np.ndarray:
+    """The n-vector whose owned chunks are `part` on their ranks."""
+    ws = dist.get_world_size()
+    chunk, c0, c1 = _slice(n)
+    buf = np.zeros(chunk)
+    buf[:c1 - c0] = part
+    outs = [torch.zeros(chunk, dtype=torch.float64) for _ in range(ws)]
+    dist.all_gather(outs, torch.from_numpy(buf))
+    return torch.cat(outs).numpy()[:n]
 
 
 class Block:
@@ -121,24 +154,33 @@ def solve(block: Block, global_rows: np.ndarray, m_total: int, cfg) -> dict:
     ax_, ay_, az_ = x.copy(), y.copy(), z.copy()
     norm_a = float(np.sqrt(lam))
 
-    def kkt(bx, by, bz):
-        xm, ym, zm = bx * cs * bsc, by * rs * csc, bz * csc / cs
+    chunk, c0, c1 = _slice(n)
+    sl = slice(c0, c1)
+
+    def kkt(bx_s, by, bz_s):
+        """KKT of the bar triple; bx_s / bz_s are this rank's column slices."""
+        xm_s, ym, zm_s = bx_s * cs[sl] * bsc, by * rs * csc, bz_s * csc / cs[sl]
+        xm = _all_gather(xm_s, n)                                   # for the local A x_m
         pv = ym - O.dual_cone(ym - block.a.ax(xm) + block.rhs, block.n_eq)
-        aty = _allreduce(block.a.aty(ym))
+        aty_s = _reduce_scatter(block.a.aty(ym))
         rows = _allreduce(np.array([pv @ pv, block.rhs @ ym]))
-        dv = block.cost - aty - zm
-        bv = xm - O.box(xm - zm, block.lower, block.upper)
-        pobj = float(block.cost @ xm) + block.offset
-        zp, zn = np.maximum(zm, 0.0), np.minimum(zm, 0.0)
-        lo_t = np.where(np.isfinite(block.lower), block.lower * zp, 0.0)
-        up_t = np.where(np.isfinite(block.upper), block.upper * zn, 0.0)
-        dobj = rows[1] + float(lo_t.sum() + up_t.sum()) + block.offset
-        rp, rb, rd = np.sqrt(rows[0]) / denom, np.linalg.norm(bv) / denom, np.linalg.norm(dv) / denom
+        dv = block.cost[sl] - aty_s - zm_s
+        bv = xm_s - O.box(xm_s - zm_s, block.lower[sl], block.upper[sl])
+        zp, zn = np.maximum(zm_s, 0.0), np.minimum(zm_s, 0.0)
+        lo_t = np.where(np.isfinite(block.lower[sl]), block.lower[sl] * zp, 0.0)
+        up_t = np.where(np.isfinite(block.upper[sl]), block.upper[sl] * zn, 0.0)
+        cols = _allreduce(np.array([dv @ dv, bv @ bv, float(block.cost[sl] @ xm_s),
+                                    float(lo_t.sum() + up_t.sum())]))
+        pobj = cols[2] + block.offset
+        dobj = rows[1] + cols[3] + block.offset
+        rp, rb, rd = np.sqrt(rows[0]) / denom, np.sqrt(cols[1]) / denom, np.sqrt(cols[0]) / denom
         gap = abs(pobj - dobj)
         rg = gap / (1.0 + abs(pobj) + abs(dobj))
-        return max(rp, rb, rd, rg), pobj, (xm, ym, zm)
+        return max(rp, rb, rd, rg), pobj, (xm, ym, _all_gather(zm_s, n))
 
-    best, pobj, tri = kkt(x, y, z)
+    x_s, z_s = x[sl].copy(), z[sl].copy()
+    ax_s, az_s = x_s.copy(), z_s.copy()
+    best, pobj, tri = kkt(x_s, y, z_s)
     last_restart = epoch_min = best
     best_tri, best_obj = tri, pobj
     k = total = last_imp = restarts = 0
@@ -147,20 +189,22 @@ def solve(block: Block, global_rows: np.ndarray, m_total: int, cfg) -> dict:
         return dict(status="optimal-tolerance", iterations=0, restarts=0, objective=pobj,
                     lam=lam, x=tri[0], y=tri[1], z=tri[2], sigma=sigma)
     while total < cfg.max_iterations:
-        g = x + sigma * (_allreduce(w.a.aty(y)) - w.cost)          # Aᵀy partials: all-reduce
-        bx = O.box(g, w.lower, w.upper)
-        bz = (bx - g) / sigma
-        xt = 2.0 * bx - x
-        by = O.dual_cone(y + (1.0 / (lam * sigma)) * (w.rhs - w.a.ax(xt)), w.n_eq)  # local rows
+        p_s = _reduce_scatter(w.a.aty(y))                         # Aᵀy partials -> owners
+        g = x_s + sigma * (p_s - w.cost[sl])
+        bx_s = O.box(g, w.lower[sl], w.upper[sl])
+        bz_s = (bx_s - g) / sigma
+        xt_s = 2.0 * bx_s - x_s
+        xt = _all_gather(xt_s, n)                                   # x~ for the local rows
+        by = O.dual_cone(y + (1.0 / (lam * sigma)) * (w.rhs - w.a.ax(xt)), w.n_eq)
         t = 1.0 / (k + 2.0)
-        x = t * ax_ + (1.0 - t) * xt
+        x_s = t * ax_s + (1.0 - t) * xt_s
         y = t * ay_ + (1.0 - t) * (2.0 * by - y)
-        z = t * az_ + (1.0 - t) * (2.0 * bz - z)
+        z_s = t * az_s + (1.0 - t) * (2.0 * bz_s - z_s)
         k += 1
         total += 1
         if total % cfg.check_every:
             continue
-        res, pobj, tri = kkt(bx, by, bz)
+        res, pobj, tri = kkt(bx_s, by, bz_s)
         if res < best:
             best, best_tri, best_obj = res, tri, pobj
         if res < epoch_min * (1.0 - 1e-12):
@@ -170,12 +214,12 @@ def solve(block: Block, global_rows: np.ndarray, m_total: int, cfg) -> dict:
             status = "optimal-tolerance"
             break
         if res <= cfg.restart_beta * last_restart or total - last_imp >= cfg.restart_stall:
-            dx = np.linalg.norm(bx - ax_)
+            dx = np.sqrt(_allsum(float((bx_s - ax_s) @ (bx_s - ax_s))))
             dy = np.sqrt(_allsum(float((by - ay_) @ (by - ay_))))
             if dx > 1e-14 and dy > 1e-14 and norm_a > 0:
                 sigma *= float(np.clip((dx / (norm_a * dy * sigma)) ** cfg.sigma_damping, 0.25, 4.0))
-            ax_, ay_, az_ = bx.copy(), by.copy(), bz.copy()
-            x, y, z = bx.copy(), by.copy(), bz.copy()
+            ax_s, ay_, az_s = bx_s.copy(), by.copy(), bz_s.copy()
+            x_s, y, z_s = bx_s.copy(), by.copy(), bz_s.copy()
             k = 0
             restarts += 1
             last_restart = epoch_min = res

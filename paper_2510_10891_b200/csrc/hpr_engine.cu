@@ -364,6 +364,9 @@ struct hpr_handle {
     // row-partitioned mode (hpr_options.nccl_comm)
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
+    // owned column slice: A^T y is reduce-scattered, each rank
+    // updates columns [c0, c0 + clen) and all-gathers x~; chunk = ceil(n / world)
+    int chunk = 0, c0 = 0, clen = 0;
     int* d_flag = nullptr;                   // collective stop flag (time limit)
     int flags = 0;                           // hpr_options.flags
     bool fused = false;                      // updates as SpMV epilogues (small LPs)
@@ -617,6 +620,31 @@ constexpr ncclDataType_t nccl_type() {
     return sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
 }
 
+// Sum an n-vector of per-rank partials and leave each rank its owned chunk in
+// place (buf + c0): ncclReduceScatter over world x chunk entries; the tail
+// [n, world x chunk) is zeroed first (the products write [0, n) only).
+template <typename T>
+void reduce_scatter(hpr_handle* h, T* buf, cudaStream_t s) {
+    if (!h->comm) return;
+    const size_t npad = (size_t)h->chunk * h->world;
+    if (npad > (size_t)h->n)
+        CK(cudaMemsetAsync(buf + h->n, 0, sizeof(T) * (npad - h->n), s));
+    const ncclResult_t r = ncclReduceScatter(buf, buf + (size_t)h->rank * h->chunk, h->chunk,
+                                             nccl_type<T>(), ncclSum, h->comm, s);
+    if (r != ncclSuccess)
+        fail(HPR_ERR_CUDA, std::string("ncclReduceScatter: ") + ncclGetErrorString(r));
+}
+
+// Replicate an n-vector whose owned chunks are current on their ranks.
+template <typename T>
+void all_gather(hpr_handle* h, T* buf, cudaStream_t s) {
+    if (!h->comm) return;
+    const ncclResult_t r = ncclAllGather(buf + (size_t)h->rank * h->chunk, buf, h->chunk,
+                                         nccl_type<T>(), h->comm, s);
+    if (r != ncclSuccess)
+        fail(HPR_ERR_CUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+}
+
 // deterministic ||v||^2 on the device -> host; row vectors (global_rows) are
 // summed over the ranks of a partitioned solve, column vectors are replicated
 double dev_sumsq(hpr_handle* h, const double* v, long long n, int finite_only,
@@ -837,19 +865,24 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     EpiStore<double> st{pd, nullptr};
     // the halt flag gates the loop kernels of the queued (partitioned / plain) loop only
     const int* halt = mode == 1 && (h->comm || plain_graph()) ? &h->ctrl->halt : nullptr;
+    all_gather(h, h->XM, s);          // partitioned: the owned chunks of the master bar x
     launch_spmv(h, h->F, (const double*)h->F.mval, (const double*)h->XM, st, s,
                 (const double*)nullptr, halt);
-    // partitioned: every rank uses the same slot count so the row-side sums reduce slot-wise
-    const int gr = h->comm ? ROW_GRID_MAX : row_grid(h->nf), gc = row_grid(h->n);
+    // partitioned: every rank uses the same slot counts, so the row-side sums (own
+    // rows) and column-side sums (owned columns) reduce slot-wise
+    const int c0 = h->comm ? h->c0 : 0, cl = h->comm ? h->clen : h->n;
+    const int gr = h->comm ? ROW_GRID_MAX : row_grid(h->nf);
+    const int gc = h->comm ? ROW_GRID_MAX : row_grid(h->n);
     CheckRowsArgs<T> ar{h->nf, h->n_eq, h->frow, pd, h->YM, h->rhs_m, p.BY, p.AY, h->rowpart};
     launch(k_check_rows<T>, gr, TPB, s, ar);
     allreduce(h, h->rowpart, (size_t)KR * gr, ncclFloat64, ncclSum, s);
     launch_spmv(h, h->FT, (const double*)h->FT.mval, (const double*)h->YMF, st, s,
                 (const double*)h->F.mval, halt);
-    allreduce(h, pd, h->n, ncclFloat64, ncclSum, s);
-    CheckColsArgs<T> ac{h->n, pd, h->XM, h->ZM, h->cost_m, h->lo_m, h->up_m, p.BX, p.BZ, p.AX,
-                        h->colpart};
+    reduce_scatter(h, pd, s);         // partitioned: A^T y_m on the owned columns
+    CheckColsArgs<T> ac{cl, pd + c0, h->XM + c0, h->ZM + c0, h->cost_m + c0, h->lo_m + c0,
+                        h->up_m + c0, p.BX + c0, p.BZ + c0, p.AX + c0, h->colpart};
     launch(k_check_cols<T>, gc, TPB, s, ac);
+    allreduce(h, h->colpart, (size_t)KC * gc, ncclFloat64, ncclSum, s);
     const int* tflag = nullptr;
     if (h->comm && mode == 1) {
         // partitioned: every rank's deadline verdict, MAX-reduced on the device,
@@ -861,11 +894,12 @@ void enqueue_check(hpr_handle* h, const Ptrs<T>& p, int mode, cudaStream_t s) {
     }
     launch(k_controller, 1, CTRL_TPB, s, h->ctrl, (const double*)h->rowpart, gr,
            (const double*)h->colpart, gc, h->log, mode, tflag);
-    const int len = std::max(h->n, h->m);
-    launch(k_restart_copy<T>, row_grid(len), TPB, s, (const Ctrl*)h->ctrl, h->n, h->m, h->nf,
-           (const double*)h->XM, (const double*)h->YM, (const double*)h->ZM, h->BXm, h->BYm,
-           h->BZm, p.X, p.Y, p.Z, p.AX, p.AY, p.AZ, (const T*)p.BX, (const T*)p.BY,
-           (const T*)p.BZ, p.YF, (const T*)p.BYF);
+    const int len = std::max(cl, h->m);
+    launch(k_restart_copy<T>, row_grid(len), TPB, s, (const Ctrl*)h->ctrl, cl, h->m, h->nf,
+           (const double*)h->XM + c0, (const double*)h->YM, (const double*)h->ZM + c0,
+           h->BXm + c0, h->BYm, h->BZm + c0, p.X + c0, p.Y, p.Z + c0, p.AX + c0, p.AY,
+           p.AZ + c0, (const T*)p.BX + c0, (const T*)p.BY, (const T*)p.BZ + c0, p.YF,
+           (const T*)p.BYF);
     h->launches += 4;
 }
 
@@ -888,11 +922,16 @@ void enqueue_iteration_t(hpr_handle* h, const Ptrs<T>& p, int j, cudaStream_t s)
     }
     EpiStore<T> st{p.P, nullptr};
     launch_spmv(h, h->FT, p.ft_vals, (const T*)p.YF, st, s, p.f_vals, halt);       // A^T y
-    allreduce(h, p.P, h->n, nccl_type<T>(), ncclSum, s);                         // partials
-    PrimalArgs<T> pa{h->ctrl, j, h->n, p.P, p.X, p.Z, p.XT, p.AX, p.AZ, p.cost, p.lo, p.up,
-                     p.BX, p.BZ, h->XM, h->ZM, h->cs, h->upd_z};
+    // partitioned: reduce-scatter the A^T y partials, update the
+    // owned column slice, all-gather x~ for the row block's A x~
+    const int c0 = h->comm ? h->c0 : 0, cl = h->comm ? h->clen : h->n;
+    reduce_scatter(h, p.P, s);
+    PrimalArgs<T> pa{h->ctrl, j, cl, p.P + c0, p.X + c0, p.Z + c0, p.XT + c0, p.AX + c0,
+                     p.AZ + c0, p.cost + c0, p.lo + c0, p.up + c0, p.BX + c0, p.BZ + c0,
+                     h->XM + c0, h->ZM + c0, h->cs + c0, h->upd_z};
     pa.halt = halt;
-    launch(k_update_primal<T, CHECK>, nblk(h->n), TPB, s, pa);
+    launch(k_update_primal<T, CHECK>, nblk(cl), TPB, s, pa);
+    all_gather(h, p.XT, s);
     launch_spmv(h, h->F, p.f_vals, (const T*)p.XT, st, s, (const T*)nullptr, halt);  // A x~
     DualArgs<T> da{h->ctrl, j, h->m, h->n_eq, h->rmap, p.P, p.Y, p.AY, p.rhs, p.YF,
                    p.BY, p.BYF, h->YM, h->YMF, h->rs};
@@ -1228,6 +1267,8 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     st->power_converged = pconv;
     st->checks = hc.checks;
     h->last_prec = fp32 ? HPR_FP32 : HPR_FP64;
+    all_gather(h, h->BXm, s);         // partitioned: the owned chunks of the best x, z
+    all_gather(h, h->BZm, s);
     if (xo) get_vec(h, xo, h->BXm, n, false);
     if (yo) get_vec(h, yo, h->BYm, m, true);
     if (zo) get_vec(h, zo, h->BZm, n, false);
@@ -1425,11 +1466,17 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
             h->comm = (ncclComm_t)opt->nccl_comm;
             h->world = std::max(1, opt->world_size);
             h->rank = opt->rank;
+            // the column vectors carry a 64-byte tail pad, so a padded chunk fits up
+            // to 8 ranks (one box; NVSwitch)
+            if (h->world > 8) fail(HPR_ERR_INVALID, "partitioned solve: at most 8 ranks");
         }
         hpr::DeviceScope dscope_(h->dev);
         CK(dscope_.err);
         h->m = p->m;
         h->n = p->n;
+        h->chunk = (p->n + h->world - 1) / h->world;
+        h->c0 = std::min(p->n, h->rank * h->chunk);
+        h->clen = std::min(p->n, h->c0 + h->chunk) - h->c0;
         h->n_eq = p->n_eq;
         h->nnz = p->nnz;
         h->offset = p->offset;
