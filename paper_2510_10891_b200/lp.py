@@ -154,6 +154,8 @@ def lazy_csc_matrix(cls, matrix):
             "__init__": __init__,
             "csc": property(_csc),
             "_t": property(lambda self: _csc(self).T),
+            # pickles (and copies through pickle) as the caller's own class
+            "__reduce__": lambda self: (cls, (self.csr,)),
             "__module__": cls.__module__,
             "__doc__": cls.__doc__,
         })
