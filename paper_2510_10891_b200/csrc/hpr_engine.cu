@@ -99,13 +99,14 @@ inline int nblk(long long n, int tpb = TPB) {
 // Fused iteration: the row-wise updates run as the epilogues of the two
 // products (2 kernels per iteration instead of 4; EpiPrimal / EpiDual, held to
 // 32 registers so the products keep 16 CTAs/SM).  Same operations, same bits.
-// Measured per iteration: C1 21.9 -> 19.3 us, C2 + 500 triples 15.7 -> 13.5,
-// C3 + 2000 triples 62.7 -> 60.4, C4 174.2 -> 174.1.  The fused kernels are
-// slower than the split pair (C4: 83.6 vs 61.4 + 14.6 us), so the win is the
-// two saved kernel boundaries, which stops paying at C4 size: fused is chosen
-// below FUSED_MAX_TILES tiles per product.  HPR_FUSED=0/1 forces the choice
-// (the partitioned mode is always split: A^T y is all-reduced first).
-constexpr int FUSED_MAX_TILES = 20000;
+// Round 1 measured, per iteration: C1 21.9 -> 19.3 us, C2 + 500 triples 15.7 ->
+// 13.5, C3 + 2000 triples 62.7 -> 60.4, C4 174.2 -> 174.1, and fused only below
+// 20,000 tiles per product.  With the round-2 tiles (256-row stream tiles,
+// column-per-thread panels) the fused pair also wins at C3 (60.7 -> 56.9 us)
+// and C4 (152.0 -> 145.4 us FP64, 120.2 -> 108.3 us FP32; tools/gpu_r2aa.sh,
+// r2ab.sh) and ties at C5 (1,147 vs 1,152 us), so it is the default unless the
+// operand runs its row-panel or panel kernels (C5 scale).  HPR_FUSED=0/1 forces
+// the choice (the partitioned mode is always split: A^T y is reduced first).
 static int fused_mode() {
     static const int mode = [] {
         const char* e = getenv("HPR_FUSED");
@@ -1785,9 +1786,8 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         plan_tiles(h, h->FT, n, h->nf, ft_nnz, h->panels ? h->pinfo : nullptr);
         {
             const int fm = fused_mode();
-            h->fused = !h->comm && (fm == 1 || (fm < 0 && std::max(h->F.ntiles + h->F.nrtiles,
-                                                                    h->FT.ntiles + h->FT.nptiles) <=
-                                                              FUSED_MAX_TILES));
+            h->fused = !h->comm &&
+                       (fm == 1 || (fm < 0 && h->F.nrtiles == 0 && h->FT.nptiles == 0));
         }
         phase("tiles");
         put_vec(h, h->rhs_m, p->rhs, m, true);
