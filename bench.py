@@ -462,7 +462,8 @@ def run_b200(args):
                       "iterations": res.iterations, "restarts": res.restarts,
                       "objective": res.objective, "rel_kkt": res.kkt.max_rel,
                       "loop_seconds": res.device_stats.get("loop_seconds"),
-                      "device_setup_seconds": res.device_stats.get("setup_seconds")}
+                      "device_setup_seconds": res.device_stats.get("setup_seconds"),
+                      "engine_create_seconds": res.device_stats.get("create_seconds")}
         if args.precision == "fp64":
             # the paper's setting (FP32 work precision, FP64 master check), same API
             del res, lp_host
@@ -479,6 +480,8 @@ def run_b200(args):
                                "iterations_per_s": r32.iterations / w32,
                                "status": r32.status.value, "objective": r32.objective,
                                "rel_kkt": r32.kkt.max_rel,
+                               "loop_seconds": r32.device_stats.get("loop_seconds"),
+                               "engine_create_seconds": r32.device_stats.get("create_seconds"),
                                "fp64_fallback": bool(getattr(r32, "fp64_fallback", False))}
     if rank == 0 and not args.no_screen:
         try:

@@ -459,6 +459,29 @@ constexpr int PANEL_MIN_ROW = 256;   // dense F rows that can serve a panel (PTD
 constexpr int PANEL_MIN_RUN = 8;     // consecutive flow rows per column worth a panel
 
 // scratch owned by one hpr_create call (stream-ordered pool allocations)
+// The layout scratch comes from the device's default stream-ordered pool.  With
+// the pool's default release threshold (0) every hpr_create maps its scratch
+// afresh, which measured 0.04-1.3 s per C4 create on the same box
+// (tools/time_e2e.py, HPR_VERBOSE phases); the pool keeps up to
+// HPR_SCRATCH_KEEP_MB (default 4096; C4's layout scratch fits) mapped between
+// creates instead.
+void retain_scratch_pool(int dev) {
+    static std::once_flag once[64];
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(once[dev], [dev] {
+        const char* e = getenv("HPR_SCRATCH_KEEP_MB");
+        const unsigned long long mb = e ? strtoull(e, nullptr, 10) : 4096ull;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        unsigned long long thr = mb << 20;       // the attribute is a 64-bit byte count
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        cudaGetLastError();
+    });
+}
+
 struct Scratch {
     cudaStream_t s = nullptr;
     std::vector<void*> blocks;
@@ -1141,6 +1164,16 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     const bool fp32 = sizeof(T) == 4;
     cudaStream_t s = h->stream;
     const int m = h->m, n = h->n;
+    const bool verbose = getenv("HPR_VERBOSE") != nullptr;
+    auto tp = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {          // host wall per phase (HPR_VERBOSE)
+        if (!verbose) return;
+        CK(cudaStreamSynchronize(s));
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[hpr_solve] %-14s %8.1f ms\n", name,
+                std::chrono::duration<double, std::milli>(now - tp).count());
+        tp = now;
+    };
     CK(cudaEventRecord(h->ev[0], s));
 
     double bsc, csc;
@@ -1155,6 +1188,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     if (prm->has_sigma0) sigma = prm->sigma0;
     else if (rn > 1e-12 && cn > 1e-12) sigma = rn / cn;
     else sigma = 1.0;
+    phase("scale+power");
     const double rhs_norm_m = std::sqrt(dev_sumsq(h, h->rhs_m, m, 0, true));
     const double cost_norm_m = std::sqrt(dev_sumsq(h, h->cost_m, n, 0));
     refresh_folded_values(h, fp32);
@@ -1210,6 +1244,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
     enqueue_check<T>(h, p, 0, s);               // initial residual (hprlp.py:371-391)
     CK(cudaEventRecord(h->ev[1], s));
     read_ctrl(h);
+    phase("init+check");
 
     const double elapsed =
         prm->time_elapsed +
@@ -1244,8 +1279,10 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
             st->loop_seconds = run_eager<T>(h, B);
         } else {
             ensure_graph<T>(h, p, B);
+            phase("graph");
             st->loop_seconds = run_loop(h, time_left);
         }
+        phase("loop");
         status = h->h_ctrl->status;
         iterations = h->h_ctrl->total;
         if (status == HPR_ITERATION_LIMIT) iterations = prm->max_iterations;
@@ -1281,6 +1318,7 @@ void solve_typed(hpr_handle* h, const hpr_params* prm, const double* x0, const d
         h->h_log.clear();
     }
     CK(cudaStreamSynchronize(s));
+    phase("download");
 }
 
 void check_plan(const Plan& p, long long rows, long long nnz, bool panels) {
@@ -1513,6 +1551,7 @@ int hpr_create(const hpr_problem* p, const hpr_options* opt, hpr_handle** out) {
         CK(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
         CK(cudaMallocHost(&h->h_scal, 8 * sizeof(double)));
         cudaStream_t s = h->stream;
+        retain_scratch_pool(h->dev);
         Scratch sc;
         sc.s = s;
         void* tmp = nullptr;

@@ -1,11 +1,14 @@
 """Split of the end-to-end hprlp.solve time at C4 (bench.py e2e): Engine()
-(upload + device layout), solve_raw (device setup + loop + copy back)."""
+(upload + device layout), solve_raw (device setup + loop + copy back).
+Usage: time_e2e.py [fp64|fp32]; HPR_VERBOSE=1 adds the per-phase host times."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2510_10891_b200 import hprlp, scuc
 doc, mon, lpa = scuc.build_config("C4")
-cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, max_iterations=200000)
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp64"
+cfg = hprlp.SolverConfig(tolerance=1e-4, ruiz=False, max_iterations=200000,
+                         precision=hprlp.Precision(prec))
 for rep in range(2):
     lp = lpa.to_lp()
     torch.cuda.synchronize()
