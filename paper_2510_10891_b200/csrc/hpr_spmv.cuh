@@ -19,10 +19,11 @@
 //    order — deterministic — and emits the row.  A slice whose columns are
 //    consecutive is streamed without its index array (taux).
 //
-// Kept deliberately lean (32 registers, 8 CTAs/SM): the projection /
-// Halpern update runs as a separate coalesced row-wise pass (hpr_update.cuh).
-// Fusing it as an SpMV epilogue was measured slower on B200 (occupancy
-// halved by the epilogue's operands).
+// Kept deliberately lean (32 registers, 16 CTAs/SM of 128 threads).  The
+// projection / Halpern updates run either as the epilogue `Epi::apply` of
+// each row (EpiPrimal / EpiDual, hpr_update.cuh: the default up to C4 scale)
+// or as separate coalesced row-wise passes (the split iteration); both give
+// the same bits.
 #pragma once
 
 #include "hpr_common.cuh"
