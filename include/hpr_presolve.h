@@ -7,8 +7,9 @@
  * reference's FIFO order so the reduced model is bit-identical (the fixing
  * decisions of successive fixing depend on it).  The numpy reductions of
  * _activity / _process_row (np.sum) are reproduced with numpy's pairwise
- * summation.  milp_presolve / lp_presolve (presolve.py:212-288) keep their
- * Python assembly (paper_2510_10891_b200/presolve.py) on top of this core.
+ * summation.  milp_presolve / lp_presolve (presolve.py:212-288) assemble the
+ * reduced model (paper_2510_10891_b200/presolve.py) from this core's output,
+ * with the reduced matrix cut by hpr_presolve_reduce.
  *
  * Host-only (no CUDA calls); exported by libhprlp_b200.so.
  */
@@ -37,8 +38,8 @@ typedef struct hpr_ps_problem {
     const int64_t* indptr;      /* CSR of A (m + 1), float64 values, sorted columns */
     const int32_t* indices;
     const double* data;
-    const int64_t* col_ptr;     /* CSC row lists (n + 1): rows of column j ascending */
-    const int32_t* col_rows;
+    const int64_t* col_ptr;     /* CSC row lists (n + 1): rows of column j ascending, */
+    const int32_t* col_rows;    /* or both NULL: built from the CSR pattern */
     const double* rhs;          /* m */
     const double* lower;        /* n (copied; the result holds the tightened bounds) */
     const double* upper;
@@ -66,6 +67,17 @@ int hpr_presolve_fetch(const hpr_ps_result* r, uint8_t* alive_row, double* lower
                        int32_t* change_col, double* change_bounds, int32_t* removed_row,
                        int8_t* removed_reason);
 void hpr_presolve_free(hpr_ps_result* r);
+
+/* The reduced matrix of milp_presolve / lp_presolve (presolve.py:238-245,
+ * :275-279: A[kept_rows][:, kept_cols] with ascending index arrays): rows with
+ * keep_row[i], columns with keep_col[j] (NULL keeps all) renumbered by rank,
+ * entries in their original order -- the arrays scipy's fancy indexing
+ * returns.  out_indices / out_data hold up to indptr[m] entries, out_indptr
+ * (kept rows + 1).  Returns -2 when the result needs int64 indices. */
+int hpr_presolve_reduce(int32_t m, int32_t n, const int64_t* indptr, const int32_t* indices,
+                        const double* data, const uint8_t* keep_row, const uint8_t* keep_col,
+                        int32_t* out_indptr, int32_t* out_indices, double* out_data,
+                        int64_t* out_nnz);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_crea
            "hpr_nccl_comm_destroy",
            # include/hpr_presolve.h (host-only presolve core)
            "hpr_presolve_run", "hpr_presolve_info", "hpr_presolve_fetch", "hpr_presolve_free",
+           "hpr_presolve_reduce",
            # include/hpr_screen.h (device flow screen)
            "hpr_screen_create", "hpr_screen_run", "hpr_screen_fetch", "hpr_screen_flows",
            "hpr_screen_bench", "hpr_screen_info_get", "hpr_screen_destroy",
@@ -153,6 +154,7 @@ def load(path: str | None = None):
     lib.hpr_presolve_fetch.argtypes = [_p] * 8
     lib.hpr_presolve_free.argtypes = [_p]
     lib.hpr_presolve_free.restype = None
+    lib.hpr_presolve_reduce.argtypes = [C.c_int32, C.c_int32] + [_p] * 8 + [C.POINTER(C.c_int64)]
     lib.hpr_screen_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.POINTER(_p), _p, C.POINTER(_p)]
     lib.hpr_screen_run.argtypes = [_p, _p, C.c_int32, C.c_double, C.POINTER(C.c_int64)]

@@ -14,6 +14,7 @@
 #include "../../include/hpr_presolve.h"
 
 #include <cmath>
+#include <cstdint>
 #include <limits>
 #include <new>
 #include <vector>
@@ -236,7 +237,8 @@ extern "C" {
 
 int hpr_presolve_run(const hpr_ps_problem* p, int32_t max_passes, hpr_ps_result** out) {
     if (!p || !out || p->m < 0 || p->n < 0 || p->n_eq < 0 || p->n_eq > p->m) return -1;
-    if ((p->m && (!p->indptr || !p->rhs)) || (p->n && (!p->lower || !p->upper || !p->col_ptr)))
+    if ((p->m && (!p->indptr || !p->rhs)) || (p->n && (!p->lower || !p->upper)) ||
+        (!p->col_ptr != !p->col_rows))
         return -1;
     hpr_ps_result* r = new (std::nothrow) hpr_ps_result();
     if (!r) return -3;
@@ -244,7 +246,33 @@ int hpr_presolve_run(const hpr_ps_problem* p, int32_t max_passes, hpr_ps_result*
         r->alive.assign(p->m, 1);
         r->lower.assign(p->lower, p->lower + p->n);
         r->upper.assign(p->upper, p->upper + p->n);
-        Reducer red(*p, *r);
+        // no CSC given: the row lists of every column, rows ascending -- the
+        // pattern of scipy's csr.tocsc() (the reference's SparseMatrix.csc,
+        // lp_kernel.py:52-62) by one counting pass, without its values
+        hpr_ps_problem q = *p;
+        std::vector<int64_t> cptr;
+        std::vector<int32_t> crow;
+        if (!p->col_ptr) {
+            cptr.assign((size_t)p->n + 1, 0);
+            const int64_t nnz = p->m ? p->indptr[p->m] : 0;
+            for (int64_t e = 0; e < nnz; ++e) {
+                const int32_t j = p->indices[e];
+                if (j < 0 || j >= p->n) {
+                    delete r;
+                    return -1;
+                }
+                ++cptr[(size_t)j + 1];
+            }
+            for (int32_t j = 0; j < p->n; ++j) cptr[(size_t)j + 1] += cptr[j];
+            crow.resize((size_t)nnz);
+            std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+            for (int32_t i = 0; i < p->m; ++i)
+                for (int64_t e = p->indptr[i]; e < p->indptr[i + 1]; ++e)
+                    crow[(size_t)fill[p->indices[e]]++] = i;
+            q.col_ptr = cptr.data();
+            q.col_rows = crow.data();
+        }
+        Reducer red(q, *r);
         red.run(max_passes);
         r->info.n_changes = (int64_t)r->ch_col.size();
         r->info.n_removed = (int64_t)r->rm_row.size();
@@ -280,5 +308,37 @@ int hpr_presolve_fetch(const hpr_ps_result* r, uint8_t* alive_row, double* lower
 }
 
 void hpr_presolve_free(hpr_ps_result* r) { delete r; }
+
+int hpr_presolve_reduce(int32_t m, int32_t n, const int64_t* indptr, const int32_t* indices,
+                        const double* data, const uint8_t* keep_row, const uint8_t* keep_col,
+                        int32_t* out_indptr, int32_t* out_indices, double* out_data,
+                        int64_t* out_nnz) {
+    if (m < 0 || n < 0 || !out_nnz || (m && (!indptr || !keep_row || !out_indptr))) return -1;
+    std::vector<int32_t> newcol;
+    if (keep_col) {                         // rank of each kept column; -1 = dropped
+        newcol.resize((size_t)n);
+        int32_t k = 0;
+        for (int32_t j = 0; j < n; ++j) newcol[j] = keep_col[j] ? k++ : -1;
+    }
+    int64_t w = 0;
+    int32_t r = 0;
+    out_indptr[0] = 0;
+    for (int32_t i = 0; i < m; ++i) {
+        if (!keep_row[i]) continue;
+        for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+            const int32_t j = indices[e];
+            if (j < 0 || j >= n) return -1;
+            const int32_t c = keep_col ? newcol[j] : j;
+            if (c < 0) continue;
+            if (w >= INT32_MAX) return -2;      // the caller keeps scipy's int64 path
+            out_indices[w] = c;
+            out_data[w] = data[e];
+            ++w;
+        }
+        out_indptr[++r] = (int32_t)w;
+    }
+    *out_nnz = w;
+    return 0;
+}
 
 }  // extern "C"

@@ -5,9 +5,13 @@ csrc/hpr_presolve.cpp).
 ``milp_presolve`` / ``lp_presolve`` take and return the caller's own model
 classes (the reference's ``MilpModel`` / ``StandardFormLp`` / ``SparseMatrix``
 when called from the reference's fixing loop or B&B, this package's mirrors
-otherwise) and assemble the reduced model with the same numpy / scipy
-operations as presolve.py:212-288, so the reduced model, the reduction log and
-the infeasibility messages are identical to the reference's.
+otherwise) and assemble the reduced model as presolve.py:212-288 does, so the
+reduced model, the reduction log and the infeasibility messages are identical
+to the reference's.  The two matrix steps the reference leaves to scipy run
+natively too: the core derives the column row-lists from the CSR pattern
+(scipy's ``tocsc``, 1.6 s per call at C4) and ``hpr_presolve_reduce`` cuts
+``A[rows][:, cols]`` in one pass (0.9 s in scipy), returning the arrays scipy's
+fancy indexing would.
 ``hprlp.install()`` rebinds them into ``scuckit.presolve``, ``scuckit.fixing``
 and ``scuckit.milp_bb``.
 """
@@ -88,8 +92,8 @@ class _Reduction:
 
     def __init__(self, lp, integrality):
         lib = _capi.load()
-        self.csr = lp.matrix.csr.astype(np.float64)
-        csc = lp.matrix.csc
+        self._lib = lib
+        self.csr = lp.matrix.csr.astype(np.float64, copy=False)   # read only
         self.rhs = lp.rhs.astype(np.float64).copy()
         self.cost = lp.cost.astype(np.float64)
         lower = np.ascontiguousarray(lp.lower, dtype=np.float64)
@@ -101,9 +105,9 @@ class _Reduction:
         keep = [np.ascontiguousarray(self.csr.indptr, dtype=np.int64),
                 np.ascontiguousarray(self.csr.indices, dtype=np.int32),
                 np.ascontiguousarray(self.csr.data, dtype=np.float64),
-                np.ascontiguousarray(csc.indptr, dtype=np.int64),
-                np.ascontiguousarray(csc.indices, dtype=np.int32),
+                None, None,              # column row-lists: built by the core
                 np.ascontiguousarray(self.rhs), lower, upper]
+        self._arrays = keep[:3]
         integ = None
         if integrality is not None:
             integ = np.ascontiguousarray(np.asarray(integrality, dtype=bool), dtype=np.uint8)
@@ -140,6 +144,34 @@ class _Reduction:
         self.removed = [(int(i), _REASONS[w]) for i, w in zip(rrow.tolist(), rwhy.tolist())]
         self.visits = int(info.visits)
         self.infeasible = self._certificate(info)
+
+    def submatrix(self, rows_mask, cols_mask=None):
+        """``csr[rows][:, cols]`` for boolean masks, as scipy's CSR (int32 index
+        arrays as scipy would pick for this size; the scipy call itself when
+        the result needs int64 indices)."""
+        import scipy.sparse as sp
+        indptr, indices, data = self._arrays
+        rows_mask = np.ascontiguousarray(rows_mask, dtype=np.uint8)
+        cmask = None if cols_mask is None else np.ascontiguousarray(cols_mask, dtype=np.uint8)
+        nr = int(np.count_nonzero(rows_mask))
+        nc = self.n if cmask is None else int(np.count_nonzero(cmask))
+        cap = int(indptr[-1]) if indptr.size else 0
+        optr = np.empty(nr + 1, dtype=np.int32)
+        oidx = np.empty(max(cap, 1), dtype=np.int32)
+        oval = np.empty(max(cap, 1), dtype=np.float64)
+        nnz = C.c_int64(0)
+        P = lambda a: None if a is None else a.ctypes.data   # noqa: E731
+        code = self._lib.hpr_presolve_reduce(self.m, self.n, P(indptr), P(indices), P(data),
+                                             P(rows_mask), P(cmask), P(optr), P(oidx), P(oval),
+                                             C.byref(nnz))
+        if code == -2:
+            rows = np.flatnonzero(rows_mask)
+            sub = self.csr[rows]
+            return sub if cmask is None else sub[:, np.flatnonzero(cmask)]
+        if code != 0:
+            raise ValueError("hpr_presolve_reduce rejected the matrix")
+        k = int(nnz.value)
+        return sp.csr_matrix((oval[:k], oidx[:k], optr), shape=(nr, nc))
 
     def _certificate(self, info):
         """The reference's infeasibility message (presolve.py:116-118, 133-148)."""
@@ -188,7 +220,7 @@ def milp_presolve(model):
     log.objective_delta = float(red.cost[fixed] @ fixed_at[fixed])
     shift = (red.csr @ np.where(fixed, fixed_at, 0.0)) if fixed.any() else np.zeros(lp.n_rows)
     reduced_lp = type(lp)(
-        matrix=lazy_csc_matrix(type(lp.matrix), red.csr[rows][:, cols]),
+        matrix=lazy_csc_matrix(type(lp.matrix), red.submatrix(red.alive_row, ~fixed)),
         rhs=(red.rhs - shift)[rows],
         cost=red.cost[cols].copy(),
         lower=red.lower[cols],
@@ -214,7 +246,7 @@ def lp_presolve(lp):
     rows = np.flatnonzero(red.alive_row)
     log.kept_rows = rows.astype(np.int64)
     reduced = type(lp)(
-        matrix=lazy_csc_matrix(type(lp.matrix), red.csr[rows]),
+        matrix=lazy_csc_matrix(type(lp.matrix), red.submatrix(red.alive_row)),
         rhs=red.rhs[rows],
         cost=red.cost.copy(),
         lower=red.lower,

@@ -62,6 +62,8 @@ def _same(a, b):
     ca, cb = pa.matrix.csr, pb.matrix.csr
     assert np.array_equal(ca.indptr, cb.indptr) and np.array_equal(ca.indices, cb.indices)
     assert np.array_equal(ca.data, cb.data)
+    assert (ca.indptr.dtype, ca.indices.dtype, ca.data.dtype) == (cb.indptr.dtype,
+                                                                  cb.indices.dtype, cb.data.dtype)
     for k in ("rhs", "cost", "lower", "upper"):
         assert np.array_equal(getattr(pa, k), getattr(pb, k)), k
     assert (pa.n_eq, pa.offset, pa.row_tags, pa.col_tags) == (pb.n_eq, pb.offset, pb.row_tags,
@@ -130,3 +132,36 @@ def test_native_rejects_bad_input():
     lib = _capi.load()
     h = C.c_void_p()
     assert lib.hpr_presolve_run(None, 100, C.byref(h)) != 0
+
+
+def test_native_submatrix_matches_scipy_fancy_indexing():
+    """hpr_presolve_reduce returns exactly csr[rows][:, cols] (presolve.py:244,
+    :278): same arrays, same dtypes, including empty selections, empty rows
+    and a matrix whose column row-lists the core builds itself."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(7)
+    for trial in range(12):
+        m, n = int(rng.integers(0, 60)), int(rng.integers(1, 50))
+        a = sp.random(m, n, density=float(rng.uniform(0.0, 0.4)), random_state=trial,
+                      format="csr")
+        a.data[rng.random(a.nnz) < 0.1] = -1.5               # some repeated values
+        lp = L.StandardFormLp(matrix=L.SparseMatrix(a), rhs=np.zeros(m), cost=np.zeros(n),
+                              lower=np.zeros(n), upper=np.ones(n), n_eq=0)
+        red = P._Reduction(lp, None)
+        rows = rng.random(m) < rng.uniform(0.0, 1.0)
+        cols = rng.random(n) < rng.uniform(0.0, 1.0)
+        if trial == 0:
+            rows[:] = False
+        if trial == 1:
+            cols[:] = False
+        ref = red.csr[np.flatnonzero(rows)][:, np.flatnonzero(cols)]
+        got = red.submatrix(rows, cols)
+        assert got.shape == ref.shape
+        for k in ("indptr", "indices", "data"):
+            x, y = getattr(got, k), getattr(ref, k)
+            assert x.dtype == y.dtype and np.array_equal(x, y), (trial, k)
+        ref = red.csr[np.flatnonzero(rows)]
+        got = red.submatrix(rows)
+        for k in ("indptr", "indices", "data"):
+            x, y = getattr(got, k), getattr(ref, k)
+            assert x.dtype == y.dtype and np.array_equal(x, y), (trial, k)
