@@ -235,7 +235,12 @@ int hpr_get_layout(hpr_handle* h, hpr_layout* out);
  * (projection + reflection + Halpern); 3: dual row-wise update; 4: one KKT
  * check block (mutates the solver state: call after the measurements);
  * 5: A^T y product with the primal update as epilogue; 6: A x~ product with the
- * dual update as epilogue (the fused iteration's two kernels). */
+ * dual update as epilogue (the fused iteration's two kernels).
+ * which | HPR_BENCH_IN_ITERATION (0..3, 5, 6): each timed launch is followed by
+ * the iteration's other kernels, untimed (5 <-> 6; 0..3: the other three), so
+ * the caches hold what they hold inside the loop; the time is the sum of the
+ * per-launch CUDA-event intervals. */
+#define HPR_BENCH_IN_ITERATION 0x100
 int hpr_resume(hpr_handle* h, int64_t more_iterations, double tolerance, hpr_stats* stats);
 int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds_per_launch);
 

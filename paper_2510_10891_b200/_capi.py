@@ -22,6 +22,7 @@ HPR_FLAG_NO_REORDER = 1
 HPR_FLAG_NO_FOLD = 2
 HPR_FLAG_NO_RUNS = 4
 HPR_FLAG_NO_PANELS = 8
+HPR_BENCH_IN_ITERATION = 0x100      # hpr_bench_kernel: time the kernel inside its iteration
 HPR_ERR_INVALID, HPR_ERR_CUDA, HPR_ERR_NOMEM, HPR_ERR_EMPTY, HPR_ERR_POWER_NULL = -1, -2, -3, -4, -5
 
 EXPORTS = ("hpr_abi_version", "hpr_last_error", "hpr_workspace_bytes", "hpr_create",

@@ -2168,14 +2168,17 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     API_BEGIN
     if (!h || !seconds_per_launch || reps < 1) fail(HPR_ERR_INVALID, "bad argument");
     if (h->last_prec < 0) fail(HPR_ERR_INVALID, "hpr_bench_kernel needs a prior solve");
+    const bool in_iter = (which & HPR_BENCH_IN_ITERATION) != 0;
+    which &= ~HPR_BENCH_IN_ITERATION;
     if (which < 0 || which > 6) fail(HPR_ERR_INVALID, "unknown kernel");
+    if (in_iter && which == 4) fail(HPR_ERR_INVALID, "the check block has no in-iteration form");
     hpr::DeviceScope dscope_(h->dev);
     CK(dscope_.err);
     cudaStream_t s = h->stream;
     // which: 0 = A x~ product, 1 = A^T y product, 2 = primal update, 3 = dual update,
     //        4 = one whole KKT check (2 master products, row/col terms, controller, copies;
     //            mutates the solver state — call last)
-    auto body = [&](auto tag) {
+    auto body = [&](auto tag, int which) {
         using T = decltype(tag);
         Ptrs<T> p = ptrs<T>(h);
         EpiStore<T> st{p.P, nullptr};
@@ -2210,18 +2213,51 @@ int hpr_bench_kernel(hpr_handle* h, int32_t which, int32_t reps, double* seconds
     // a finished solve leaves Ctrl::halt set; the loop kernels timed here
     // must not take their halted (no-op) path
     CK(cudaMemsetAsync(&h->ctrl->halt, 0, sizeof(int), s));
-    auto run = [&]() {
-        if (h->last_prec == HPR_FP32) body(float(0));
-        else body(double(0));
+    auto run = [&](int w) {
+        if (h->last_prec == HPR_FP32) body(float(0), w);
+        else body(double(0), w);
     };
-    run();  // warm
-    CK(cudaEventRecord(h->ev[0], s));
-    for (int r = 0; r < reps; ++r) run();
-    CK(cudaEventRecord(h->ev[1], s));
-    CK(cudaEventSynchronize(h->ev[1]));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
-    *seconds_per_launch = ms * 1e-3 / reps;
+    // the rest of the iteration, in loop order after `which`
+    std::vector<int> rest;
+    if (in_iter) {
+        if (which >= 5) rest = {which == 5 ? 6 : 5};
+        else for (int k = 1; k < 4; ++k) rest.push_back((which + k) % 4);
+    }
+    run(which);  // warm
+    for (int w : rest) run(w);
+    if (!in_iter) {
+        CK(cudaEventRecord(h->ev[0], s));
+        for (int r = 0; r < reps; ++r) run(which);
+        CK(cudaEventRecord(h->ev[1], s));
+        CK(cudaEventSynchronize(h->ev[1]));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+        *seconds_per_launch = ms * 1e-3 / reps;
+    } else {
+        std::vector<cudaEvent_t> ev(2 * (size_t)reps, nullptr);
+        struct Release {
+            std::vector<cudaEvent_t>& v;
+            ~Release() {
+                for (cudaEvent_t e : v)
+                    if (e) cudaEventDestroy(e);
+            }
+        } release_{ev};
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        for (int r = 0; r < reps; ++r) {
+            CK(cudaEventRecord(ev[2 * r], s));
+            run(which);
+            CK(cudaEventRecord(ev[2 * r + 1], s));
+            for (int w : rest) run(w);
+        }
+        CK(cudaEventSynchronize(ev.back()));
+        double total = 0.0;
+        for (int r = 0; r < reps; ++r) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+            total += ms;
+        }
+        *seconds_per_launch = total * 1e-3 / reps;
+    }
     API_END
 }
 

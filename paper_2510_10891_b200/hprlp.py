@@ -324,13 +324,15 @@ class Engine:
         _capi.check(self._lib.hpr_get_layout(self._h, _capi.C.byref(lay)))
         return {k: getattr(lay, k) for k, _ in lay._fields_}
 
-    def bench_kernel(self, which: int, reps: int = 20) -> float:
+    def bench_kernel(self, which: int, reps: int = 20, in_iteration: bool = False) -> float:
         """Average device seconds of one iteration kernel (hpr_bench_kernel:
         0: A x~ product, 1: A^T y product, 2: primal update, 3: dual update,
-        4: one KKT check block)."""
+        4: one KKT check block, 5 / 6: the fused pair).  `in_iteration`: each
+        timed launch is followed by the iteration's other kernels, so the
+        caches hold what they hold in the loop."""
         sec = _capi.C.c_double()
-        _capi.check(self._lib.hpr_bench_kernel(self._h, int(which), int(reps),
-                                               _capi.C.byref(sec)))
+        w = int(which) | (_capi.HPR_BENCH_IN_ITERATION if in_iteration else 0)
+        _capi.check(self._lib.hpr_bench_kernel(self._h, w, int(reps), _capi.C.byref(sec)))
         return sec.value
 
     def solve_raw(self, config, start=None, time_elapsed=0.0, rows=None, m_total=None):

@@ -17,6 +17,8 @@ ap.add_argument("--precision", default="fp64")
 ap.add_argument("--reorder", type=int, default=1)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--which", default="0,1,2,3")
+ap.add_argument("--in-iteration", action="store_true",
+                help="follow each timed launch by the rest of its iteration (loop cache state)")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -34,7 +36,7 @@ torch.cuda.synchronize()
 out = []
 with torch.cuda.nvtx.range("iter"):
     for w in [int(v) for v in a.which.split(",")]:
-        out.append(f"{NAMES[w]} {eng.bench_kernel(w, a.reps) * 1e6:.1f} us")
+        out.append(f"{NAMES[w]} {eng.bench_kernel(w, a.reps, in_iteration=a.in_iteration) * 1e6:.1f} us")
 torch.cuda.synchronize()
 print(f"{os.environ.get('HPR_LIB', 'default')} {a.config} {a.precision} {lpa.shape} "
       f"nnz={lpa.nnz} | " + " | ".join(out))
