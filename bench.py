@@ -340,16 +340,20 @@ def run_b200(args):
         st = eng.resume(args.steps * BLOCK, tolerance=1e-300)
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_pop()
-        # per-kernel times: CUDA events around each launch, every launch followed
-        # by the rest of its iteration, so L2 holds what it holds in the loop
-        split = {name: eng.bench_kernel(which, args.kernel_reps, in_iteration=True)
-                 for name, which in (("spmv_A", 0), ("spmv_AT", 1), ("update_primal", 2),
-                                     ("update_dual", 3))}
+        # per-kernel times: back-to-back launches between two CUDA events on the
+        # engine stream (the launch latency hidden as in the loop's graph)
+        names = (("spmv_A", 0), ("spmv_AT", 1), ("update_primal", 2), ("update_dual", 3))
+        split = {name: eng.bench_kernel(which, args.kernel_reps) for name, which in names}
         fused = bool(lay.get("fused"))
         # the kernels the loop actually runs: the fused iteration has two
-        ktimes = ({name: eng.bench_kernel(which, args.kernel_reps, in_iteration=True)
-                   for name, which in (("spmv_AT+primal", 5), ("spmv_A+dual", 6))}
+        loop_names = (("spmv_AT+primal", 5), ("spmv_A+dual", 6)) if fused else names
+        ktimes = ({name: eng.bench_kernel(which, args.kernel_reps) for name, which in loop_names}
                   if fused else dict(split))
+        # upper bounds: events around every launch, each launch followed by the rest
+        # of its iteration (the loop's cache state, but each interval also holds
+        # the launch ramp that the back-to-back form and the graph hide)
+        k_in_iter = {name: eng.bench_kernel(which, args.kernel_reps, in_iteration=True)
+                     for name, which in loop_names}
         t_check = eng.bench_kernel(4, 4)     # one KKT check block (mutates state: last)
     if ws > 1:
         torch.distributed.barrier()
@@ -418,9 +422,9 @@ def run_b200(args):
                                "frac": stored[k] / t / 1e9 / peak}
                            for k, t in split.items()} if fused else None),
         "iteration_kernels": "fused (updates as SpMV epilogues)" if fused else "split",
-        "kernel_timing": "CUDA events around each launch on the engine stream; each timed "
-                         "launch followed by the rest of its iteration (hpr_bench_kernel "
-                         "HPR_BENCH_IN_ITERATION)",
+        "kernel_timing": "back-to-back launches of each kernel between two CUDA events on "
+                         "the engine stream (hpr_bench_kernel)",
+        "kernels_in_iteration_us": {k: 1e6 * t for k, t in k_in_iter.items()},
         "iteration_us": 1e6 * t_loop / its,
         "kernel_sum_us": 1e6 * sum(ktimes.values()),
         "check_block_us": 1e6 * t_check,
