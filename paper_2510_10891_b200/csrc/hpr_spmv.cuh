@@ -28,6 +28,12 @@
 
 #include "hpr_common.cuh"
 
+// stream tiles hand a thread's two rows to Epi::apply2 in one call
+// (-DHPR_PAIR_EPI=0: row by row, for A/B)
+#ifndef HPR_PAIR_EPI
+#define HPR_PAIR_EPI 1
+#endif
+
 namespace hpr {
 
 template <int K>
@@ -171,12 +177,29 @@ __global__ void __launch_bounds__(TPB, Epi::MIN_CTAS) k_spmv(Csr<T> A, const T* 
         const int grp = threadIdx.x / L;
         const int ngrp = TPB / L;
         const unsigned mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane & ~(L - 1)));
-        for (int k = grp; k < R; k += ngrp) {
-            const int b = sptr[k], e = sptr[k + 1];
-            T s = T(0);
-            for (int q = b + gl; q < e; q += L) s += prod[q];
-            for (int off = L >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(mask, s, off);
-            if (gl == 0) epi.apply(r0 + k, s, acc);
+        bool done = false;
+        if constexpr (Epi::PAIR && TILE_ROWS == 2 * TPB && HPR_PAIR_EPI) {
+            if (L == 1) {
+                // rows k and k + TPB of this thread: both sums (index order, as
+                // the loop below), then one epilogue call for the two rows
+                const int k0 = threadIdx.x, k1 = threadIdx.x + TPB;
+                T s0 = T(0), s1 = T(0);
+                if (k0 < R)
+                    for (int q = sptr[k0]; q < sptr[k0 + 1]; ++q) s0 += prod[q];
+                if (k1 < R)
+                    for (int q = sptr[k1]; q < sptr[k1 + 1]; ++q) s1 += prod[q];
+                epi.apply2(r0 + k0, s0, k0 < R, r0 + k1, s1, k1 < R, acc);
+                done = true;
+            }
+        }
+        if (!done) {
+            for (int k = grp; k < R; k += ngrp) {
+                const int b = sptr[k], e = sptr[k + 1];
+                T s = T(0);
+                for (int q = b + gl; q < e; q += L) s += prod[q];
+                for (int off = L >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(mask, s, off);
+                if (gl == 0) epi.apply(r0 + k, s, acc);
+            }
         }
         block_store<Epi::K>(acc, epi.part, A.ntiles + A.nlong, blockIdx.x);
     } else {
@@ -366,6 +389,7 @@ struct EpiStore {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
     static constexpr bool ROW_PANELS = true, COL_PANELS = true;   // F and F^T
+    static constexpr bool PAIR = false;
     T* out;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { out[r] = s; }
@@ -376,6 +400,7 @@ struct EpiPower {
     static constexpr int K = 1;
     static constexpr int MIN_CTAS = 16;
     static constexpr bool ROW_PANELS = false, COL_PANELS = false; // A and A^T
+    static constexpr bool PAIR = false;
     double* out;
     double* part;
     __device__ __forceinline__ void apply(int r, double s, Acc<1>& a) {

@@ -88,6 +88,7 @@ struct EpiPrimal {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
     static constexpr bool ROW_PANELS = false, COL_PANELS = true;  // F^T only
+    static constexpr bool PAIR = false;  // no dependent load to batch (spills if paired)
     PrimalArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { primal_col<T, CHECK>(a, r, s); }
@@ -175,13 +176,25 @@ struct EpiDual {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
     static constexpr bool ROW_PANELS = true, COL_PANELS = false;  // F only
+    static constexpr bool PAIR = true;
     DualArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int f, T s, Acc<0>&) {
+        const int i = a.frow[f];
+        finish(f, s, i, a.frow[f + 1] - i == 2);
+    }
+    // two folded rows of one thread: both rows' frow entries in one round trip
+    __device__ __forceinline__ void apply2(int f0, T s0, bool v0, int f1, T s1, bool v1,
+                                           Acc<0>&) {
+        int i0 = 0, e0 = 0, i1 = 0, e1 = 0;
+        if (v0) { i0 = a.frow[f0]; e0 = a.frow[f0 + 1]; }
+        if (v1) { i1 = a.frow[f1]; e1 = a.frow[f1 + 1]; }
+        if (v0) finish(f0, s0, i0, e0 - i0 == 2);
+        if (v1) finish(f1, s1, i1, e1 - i1 == 2);
+    }
+    __device__ __forceinline__ void finish(int f, T s, int i, bool pair) {
         const double td = halpern_t(a.ctrl, a.j_in_block);
         const T inv = (T)(1.0 / (a.ctrl->lam * a.ctrl->sigma)), t = (T)td, omt = (T)(1.0 - td);
-        const int i = a.frow[f];
-        const bool pair = a.frow[f + 1] - i == 2;
         const DualRow<T> r = dual_row(a.Y[i], a.RHS[i], a.AY[i], s, i >= a.n_eq, inv, t, omt);
         DualRow<T> r2{T(0), T(0)};
         if (pair) {
