@@ -15,6 +15,15 @@
 
 #include "hpr_spmv.cuh"
 
+// EpiDual::apply2 also loads both rows' y / rhs / y-anchor before either row
+// stores (-DHPR_PAIR_EPI_LOADS=0: only the frow entries are paired; A/B)
+#ifndef HPR_PAIR_PRIMAL
+#define HPR_PAIR_PRIMAL 1
+#endif
+#ifndef HPR_PAIR_EPI_LOADS
+#define HPR_PAIR_EPI_LOADS 1
+#endif
+
 namespace hpr {
 
 __device__ __forceinline__ double halpern_t(const Ctrl* c, int j) {
@@ -47,6 +56,24 @@ struct PrimalArgs {
     const int* halt = nullptr;  // queued block loop only (Ctrl::halt)
 };
 
+// z's Halpern update (hpr_iterate only) and the check iteration's bars
+template <typename T, bool CHECK>
+__device__ __forceinline__ void primal_tail(const PrimalArgs<T>& a, int j, T bx, T bz, T t,
+                                            T omt) {
+    if (a.upd_z) {
+        const T zh = T(2) * bz - a.Z[j];
+        a.Z[j] = t * a.AZ[j] + omt * zh;
+    }
+    if constexpr (CHECK) {
+        const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
+        a.BX[j] = bx;
+        a.BZ[j] = bz;
+        const double cs = a.CS[j];
+        a.XM[j] = ((double)bx * cs) * bsc;
+        a.ZM[j] = ((double)bz * csc) / cs;
+    }
+}
+
 template <typename T, bool CHECK>
 __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
     const double td = halpern_t(a.ctrl, a.j_in_block);
@@ -59,17 +86,48 @@ __device__ __forceinline__ void primal_col(const PrimalArgs<T>& a, int j, T p) {
     const T xt = T(2) * bx - x;
     a.XT[j] = xt;
     a.X[j] = t * ax + omt * xt;
-    if (a.upd_z) {
-        const T zh = T(2) * bz - a.Z[j];
-        a.Z[j] = t * a.AZ[j] + omt * zh;
+    primal_tail<T, CHECK>(a, j, bx, bz, t, omt);
+}
+
+// two columns of one thread (EpiPrimal::apply2): the first column is computed,
+// the second one's operands are loaded, and only then does the first store --
+// the second column's loads do not wait behind the first one's stores (the
+// pointers may alias), and only the first column's two results stay live
+template <typename T, bool CHECK>
+__device__ __forceinline__ void primal_col2(const PrimalArgs<T>& a, int j0, T p0, bool v0,
+                                            int j1, T p1, bool v1) {
+    const double td = halpern_t(a.ctrl, a.j_in_block);
+    const T sig = (T)a.ctrl->sigma, t = (T)td, omt = (T)(1.0 - td);
+    T xt0 = T(0), bx0 = T(0), bz0 = T(0), ax0 = T(0);
+    if (v0) {
+        const T x = a.X[j0], c = a.C[j0], lo = a.LO[j0], up = a.UP[j0];
+        ax0 = a.AX[j0];
+        const T g = x + sig * (p0 - c);
+        bx0 = np_clip(g, lo, up);
+        bz0 = (bx0 - g) / sig;
+        xt0 = T(2) * bx0 - x;
     }
-    if constexpr (CHECK) {
-        const double bsc = a.ctrl->b_scale, csc = a.ctrl->c_scale;
-        a.BX[j] = bx;
-        a.BZ[j] = bz;
-        const double cs = a.CS[j];
-        a.XM[j] = ((double)bx * cs) * bsc;
-        a.ZM[j] = ((double)bz * csc) / cs;
+    T x1 = T(0), c1 = T(0), lo1 = T(0), up1 = T(0), ax1 = T(0);
+    if (v1) {
+        x1 = a.X[j1];
+        c1 = a.C[j1];
+        lo1 = a.LO[j1];
+        up1 = a.UP[j1];
+        ax1 = a.AX[j1];
+    }
+    if (v0) {
+        a.XT[j0] = xt0;
+        a.X[j0] = t * ax0 + omt * xt0;
+        primal_tail<T, CHECK>(a, j0, bx0, bz0, t, omt);
+    }
+    if (v1) {
+        const T g = x1 + sig * (p1 - c1);
+        const T bx = np_clip(g, lo1, up1);
+        const T bz = (bx - g) / sig;
+        const T xt = T(2) * bx - x1;
+        a.XT[j1] = xt;
+        a.X[j1] = t * ax1 + omt * xt;
+        primal_tail<T, CHECK>(a, j1, bx, bz, t, omt);
     }
 }
 
@@ -88,10 +146,15 @@ struct EpiPrimal {
     static constexpr int K = 0;
     static constexpr int MIN_CTAS = 16;
     static constexpr bool ROW_PANELS = false, COL_PANELS = true;  // F^T only
-    static constexpr bool PAIR = false;  // no dependent load to batch (spills if paired)
+    // paired columns: FP64 +0.6% at C4; FP32 slower (A/B), so FP64 only
+    static constexpr bool PAIR = HPR_PAIR_PRIMAL && sizeof(T) == 8;
     PrimalArgs<T> a;
     double* part;
     __device__ __forceinline__ void apply(int r, T s, Acc<0>&) { primal_col<T, CHECK>(a, r, s); }
+    __device__ __forceinline__ void apply2(int r0, T s0, bool v0, int r1, T s1, bool v1,
+                                           Acc<0>&) {
+        primal_col2<T, CHECK>(a, r0, s0, v0, r1, s1, v1);
+    }
 };
 
 // ---------------------------------------------------------------------------
@@ -181,7 +244,7 @@ struct EpiDual {
     double* part;
     __device__ __forceinline__ void apply(int f, T s, Acc<0>&) {
         const int i = a.frow[f];
-        finish(f, s, i, a.frow[f + 1] - i == 2);
+        finish<false>(f, s, i, a.frow[f + 1] - i == 2);
     }
     // two folded rows of one thread: both rows' frow entries in one round trip
     __device__ __forceinline__ void apply2(int f0, T s0, bool v0, int f1, T s1, bool v1,
@@ -189,13 +252,28 @@ struct EpiDual {
         int i0 = 0, e0 = 0, i1 = 0, e1 = 0;
         if (v0) { i0 = a.frow[f0]; e0 = a.frow[f0 + 1]; }
         if (v1) { i1 = a.frow[f1]; e1 = a.frow[f1 + 1]; }
-        if (v0) finish(f0, s0, i0, e0 - i0 == 2);
-        if (v1) finish(f1, s1, i1, e1 - i1 == 2);
+        if constexpr (HPR_PAIR_EPI_LOADS && sizeof(T) == 8) {
+            // FP64: the rows' own operands too, before either row stores
+            // (A/B: FP64 +0.55%, FP32 -0.5%, so FP32 keeps the lazier form)
+            T y0 = T(0), b0 = T(0), h0 = T(0), y1 = T(0), b1 = T(0), h1 = T(0);
+            if (v0) { y0 = a.Y[i0]; b0 = a.RHS[i0]; h0 = a.AY[i0]; }
+            if (v1) { y1 = a.Y[i1]; b1 = a.RHS[i1]; h1 = a.AY[i1]; }
+            if (v0) finish<true>(f0, s0, i0, e0 - i0 == 2, y0, b0, h0);
+            if (v1) finish<true>(f1, s1, i1, e1 - i1 == 2, y1, b1, h1);
+        } else {
+            if (v0) finish<false>(f0, s0, i0, e0 - i0 == 2);
+            if (v1) finish<false>(f1, s1, i1, e1 - i1 == 2);
+        }
     }
-    __device__ __forceinline__ void finish(int f, T s, int i, bool pair) {
+    // PRE: the row's y / rhs / anchor were loaded by the caller
+    template <bool PRE>
+    __device__ __forceinline__ void finish(int f, T s, int i, bool pair, T yi = T(0),
+                                           T rhsi = T(0), T ayi = T(0)) {
         const double td = halpern_t(a.ctrl, a.j_in_block);
         const T inv = (T)(1.0 / (a.ctrl->lam * a.ctrl->sigma)), t = (T)td, omt = (T)(1.0 - td);
-        const DualRow<T> r = dual_row(a.Y[i], a.RHS[i], a.AY[i], s, i >= a.n_eq, inv, t, omt);
+        DualRow<T> r;
+        if constexpr (PRE) r = dual_row(yi, rhsi, ayi, s, i >= a.n_eq, inv, t, omt);
+        else r = dual_row(a.Y[i], a.RHS[i], a.AY[i], s, i >= a.n_eq, inv, t, omt);
         DualRow<T> r2{T(0), T(0)};
         if (pair) {
             r2 = dual_row(a.Y[i + 1], a.RHS[i + 1], a.AY[i + 1], -s, i + 1 >= a.n_eq, inv, t, omt);
